@@ -1,0 +1,397 @@
+"""Benchmark: Feynman paths/sec of the hybrid path sum on 1..8 B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (default ``--config cfg4``, BASELINE.json configs[3] -- the config
+whose metric is quoted "paths sharded across 1/2/4/8 GPUs"): 6x7 grid,
+depth 1+32+1, 21|21 cut, f = 0.01, 10^6 seeded bitstrings.  One *step* is
+one batch of paths: every rank takes the next window of ``--window`` sorted
+retained prefixes (x all 8 branches each) from its own contiguous slice of
+the retained set, evolves them through the path tree on its GPU, gathers the
+10^6 requested amplitudes into its complex128 partial, and the ranks
+all-reduce the partials over NCCL.  Per-GPU work is fixed as N grows
+(``scaling: weak``).
+
+Every number is device-timed with CUDA events on the stream the engine
+launches on (the torch current stream, handed to the library), max over
+ranks.  ``e2e`` repeats the measurement through the public API
+(``run_batched`` / ``run_batched_sharded``) with host buffers: request upload
+and result download are inside its timed region.  ``--impl reference`` times
+the reference algorithm (the CPU oracle -- a numpy restatement of the
+reference's run_batched, because the reference is pure Python and cannot be
+installed on the GPU box) on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Feynman paths/sec (whole box)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--window", type=int, default=0, help="prefixes per GPU per step (0 = auto)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-procs", type=int, default=0)
+    return ap.parse_args()
+
+
+DEFAULT_WINDOW = {"cfg1": 16, "cfg1v2": 32, "cfg2": 32768, "cfg2v2": 32768, "cfg2h": 2048,
+                  "cfg3": 256, "cfg3v2": 128, "cfg4": 8, "cfg4v2": 4, "cfg5": 1, "cfg5v2": 1, "cfg5f": 1}
+
+
+def describe(name, plan, window, n_req):
+    from paper_1807_10749_b200.configs import CONFIGS
+
+    s = CONFIGS[name]
+    return (f"{name}: {s.rows}x{s.cols} grid, depth 1+{s.depth}+1 ({s.version}+final H), "
+            f"{plan.cut.n_a}|{plan.cut.n_b} cut, f={s.fidelity:g}, {n_req} bitstrings; "
+            f"step = {window} retained prefixes x {plan.branch_space} branches per GPU")
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of the reference's run_batched), forked over cores
+
+def _cpu_job(args):
+    name, prefixes, n_req = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import pathsum_oracle as oracle
+    from paper_1807_10749_b200 import configs
+
+    circ, plan, req, _ = configs.build(name, n_req=n_req)
+    t = time.perf_counter()
+    amps = oracle.run_batched(circ, plan, req, np.asarray(prefixes, dtype=np.int64))
+    return time.perf_counter() - t, amps
+
+
+def cpu_reference(name, prefixes, n_req, procs, pool=None):
+    """Time the reference algorithm on `procs` processes, one prefix slice each."""
+    import multiprocessing as mp
+
+    slices = [s for s in np.array_split(np.asarray(prefixes), procs) if s.size]
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(len(slices))
+    t = time.perf_counter()
+    res = pool.map(_cpu_job, [(name, s, n_req) for s in slices])
+    wall = time.perf_counter() - t
+    if own:
+        pool.close()
+    total = sum(r[1] for r in res)
+    return wall, total, len(slices)
+
+
+# ---------------------------------------------------------------------------
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return world, rank, local
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return main_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1807_10749_b200 import configs
+    from paper_1807_10749_b200.distributed import partition_prefixes, run_batched_sharded
+    from paper_1807_10749_b200.engine import ENGINES
+    from paper_1807_10749_b200.lowering import lowered
+    from paper_1807_10749_b200.pathsum import run_batched
+    from paper_1807_10749_b200.plan import split_requests
+
+    world, rank, local = dist_setup(args)
+    name = args.config
+    circ, plan, req, pre_all = configs.build(name)
+    window = args.window or DEFAULT_WINDOW.get(name, 8)
+    n_steps_total = args.warmup + args.steps
+
+    def rank_windows(r):
+        """Step s of rank r: the s-th window of r's contiguous slice (wrapping if short)."""
+        sl = partition_prefixes(pre_all, world, r)
+        if sl.size < window:
+            raise SystemExit(f"rank {r}: only {sl.size} prefixes for a window of {window}")
+        n_win = sl.size // window
+        return [sl[(s % n_win) * window:((s % n_win) + 1) * window] for s in range(n_steps_total)]
+
+    windows = rank_windows(rank)
+    all_windows = [rank_windows(r) for r in range(world)] if world > 1 else [windows]
+
+    eng = ENGINES.get(local, args.dtype)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    prog = lowered(circ, plan.cut)
+    eng.load_program(prog)
+    ia, ib = split_requests(circ.n_qubits, plan.cut.block_a, plan.cut.block_b, req)
+    eng.set_requests(ia, ib)
+    n_req = req.size
+    out = torch.zeros(2 * n_req, dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step(s, stats_acc=None):
+        flush.zero_()  # L2 flush between steps (the working set is >> L2 anyway)
+        r = eng.run(plan.x_p, windows[s], 0, plan.branch_space, out_device_ptr=out.data_ptr(),
+                    want_host=False)
+        if world > 1:
+            dist.all_reduce(out)
+        if stats_acc is not None:
+            stats_acc.append(r.stats)
+        return r.stats
+
+    for s in range(args.warmup):
+        step(s)
+    # one profiled step (events around every level) for the kernel split / roofline
+    eng.set_option("profile", 1)
+    prof = step(args.warmup % n_steps_total)
+    eng.set_option("profile", 0)
+
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stats = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for s in range(args.steps):
+            step(args.warmup + s, stats)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    paths_rank = sum(st["n_paths"] for st in stats)
+    paths = paths_rank * world  # every rank processes the same window size
+    value = paths / (ms / 1e3)
+
+    # e2e through the public API with host buffers (request upload + result download inside)
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_paths = 0
+        for s in range(args.steps):
+            w = windows[args.warmup + s]
+            if world > 1:
+                union = np.concatenate([all_windows[r][args.warmup + s] for r in range(world)])
+                res = run_batched_sharded(circ, plan, req, prefixes=union, dst=None, device=local)
+            else:
+                res = run_batched(circ, plan, req, prefixes=w, device=local)
+            e2e_paths += w.size * plan.branch_space * world
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": e2e_paths / el, "unit": "paths/s",
+               "h2d_bytes_per_step": int(8 * n_req + 8 * window + stats[-1]["h2d_bytes"]),
+               "d2h_bytes_per_step": int(16 * n_req), "timer": "host wall clock, max over ranks"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (gate_pass_kernel) from the profiled step
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    ms_pass = prof["ms_pass"]
+    launches = max(1, prof["n_pass_launches"])
+    roofline = {
+        "bound": "hbm",
+        "kernel": "gate_pass_kernel",
+        "achieved": prof["pass_bytes_min"] / (ms_pass / 1e3) / 1e9 if ms_pass else None,
+        "peak": peak,
+        "unit": "GB/s",
+        "frac": (prof["pass_bytes_min"] / (ms_pass / 1e3) / 1e9) / peak if ms_pass else None,
+        "traffic": None,
+        "algorithmic_bytes_per_launch": prof["pass_bytes_min"] / launches,
+        "avg_launch_ms": ms_pass / launches,
+        "kernel_bytes_per_launch": prof["pass_bytes"] / launches,
+        "kernel_gbs": prof["pass_bytes"] / (ms_pass / 1e3) / 1e9 if ms_pass else None,
+        "share_of_step": ms_pass / prof["ms_total"] if prof["ms_total"] else None,
+        "gather_ms": prof["ms_gather"],
+        "peak_source": peak_src,
+        "basis": "algorithmic = one read+write of both half-states per path-tree node per level "
+                 "(SURVEY.md §8d); kernel_gbs counts every pass actually made",
+    }
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "paths/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32 complex states, fp64 accumulation)" if args.dtype == "c64" else "c128",
+        "data": "synthetic: reference-generator circuit (seed 0), challenge_indices(seed 12345)",
+        "config": {
+            "workload": describe(name, plan, window, n_req),
+            "paths_per_gpu_per_step": int(paths_rank / max(1, args.steps)),
+            "l2": "256 MB L2 flush before every step; working set (16 MB half-states x nodes) >> L2",
+            "parallelism": f"path-sharded dp{world}, NCCL all-reduce of the complex128 partials",
+        },
+        "e2e": e2e,
+        "roofline": roofline,
+        "gpu_launches": int(sum(st["n_launches"] for st in stats)),
+        "clocks": clk.summary(),
+        "nodes_per_step": int(np.mean([st["n_nodes"] for st in stats])),
+    }
+    if not args.no_cpu and world == 1:
+        procs = args.cpu_procs or min(os.cpu_count() or 1, 32)
+        sample = windows[args.warmup][: max(1, min(window, procs))]
+        wall, _, used = cpu_reference(name, sample, n_req, min(procs, sample.size))
+        cpu_paths = sample.size * plan.branch_space
+        line["cpu_baseline"] = {
+            "value": cpu_paths / wall, "unit": "paths/s", "cores": used, "kind": "port",
+            "sample": f"{sample.size} prefixes x {plan.branch_space} branches of the same window, "
+                      f"{used} forked processes, numpy restatement of reference run_batched",
+        }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main_reference(args):
+    """Reference arm: the reference algorithm (oracle port) on all host cores, rank 0 only."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    from paper_1807_10749_b200 import configs
+
+    name = args.config
+    circ, plan, req, pre_all = configs.build(name)
+    procs = args.cpu_procs or min(os.cpu_count() or 1, 64)
+    per_step = procs  # one prefix (all its branches) per process per step
+    pool = mp.get_context("fork").Pool(procs)
+    times, paths = [], 0
+    for s in range(args.warmup + args.steps):
+        sample = pre_all[s * per_step:(s + 1) * per_step]
+        wall, _, used = cpu_reference(name, sample, req.size, procs, pool)
+        if s >= args.warmup:
+            times.append(wall)
+            paths += sample.size * plan.branch_space
+    pool.close()
+    total = sum(times)
+    value = paths / total
+    line = {
+        "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "impl": "reference",
+        "dtype": "c64 (numpy complex64 states, complex128 accumulation)",
+        "data": "synthetic: reference-generator circuit (seed 0), challenge_indices(seed 12345)",
+        "config": {"workload": describe(name, plan, per_step, req.size) + " (CPU: one prefix per process)",
+                   "parallelism": f"{procs} forked CPU processes"},
+        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": procs, "kind": "port",
+                         "sample": f"{per_step} prefixes x {plan.branch_space} branches per step"},
+        "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

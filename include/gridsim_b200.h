@@ -1,0 +1,138 @@
+/*
+ * gridsim_b200.h -- C ABI of the B200 Schroedinger-Feynman path-sum engine.
+ *
+ * The reference (`gridsim`, pure Python) has no FFI; its operator boundary
+ * for this hot path is the Python function
+ *
+ *     run_approx(circuit, plan, requests, skip_zeros=True, engine="batched")
+ *         -> AmplitudeBatch                       (pkg/src/gridsim/pathsum.py:419-443)
+ *
+ * whose `engine=` string dispatch (pathsum.py:433-436) and the
+ * `run_batched(..., prefixes=...)` subset hook (pathsum.py:574-579) are the
+ * only extension points.  This library replaces everything below that call:
+ * the batched op-stream executor (`_exec_ops_batched`, pathsum.py:537-557,
+ * with the `_b_*` kernels pathsum.py:450-513), the prefix checkpoint/branch
+ * replay (`run_batched` pathsum.py:617-636, `run_prefix_tree` :377-416) and
+ * the gather + complex128 multiply-accumulate (`land`, pathsum.py:607-615).
+ * Planning (cut, Schmidt terms, retained prefixes) and lowering stay on the
+ * host in the reference's Python API; the binding packs the lowered op stream
+ * (`_lower`, pathsum.py:145-195) into the flat arrays below.
+ *
+ * Conventions
+ *  - Every entry point returns GS_OK (0) or a negative GS_ERR_* code and never
+ *    throws across the boundary; gs_last_error() holds the message.
+ *  - The caller owns every host buffer; the library copies in/out and keeps no
+ *    host pointer after a call returns.
+ *  - One call in flight per context.  Calls are synchronous: when gs_run
+ *    returns, the result is in the output buffer.
+ *  - Contexts are per process and per device; create them after any fork()
+ *    (the reference orchestrator forks workers, orchestrator.py:237).
+ */
+#ifndef GRIDSIM_B200_H
+#define GRIDSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+
+/* error codes; the Python binding maps them onto the reference's exceptions */
+#define GS_OK 0
+#define GS_ERR_ARG (-1)    /* ValueError   (bad engine/digit/path id, pathsum.py:225,435,567) */
+#define GS_ERR_PLAN (-2)   /* CircuitError (split/fidelity/plan mismatch, pathsum.py:309,323) */
+#define GS_ERR_INDEX (-3)  /* IndexError   (request outside the state space, pathsum.py:131) */
+#define GS_ERR_CUDA (-4)   /* RuntimeError (CUDA failure) */
+#define GS_ERR_NOMEM (-5)  /* MemoryError  (device memory budget) */
+#define GS_ERR_STATE (-6)  /* RuntimeError (call order: no program / no requests loaded) */
+
+/* numeric modes: state amplitudes and gate arithmetic; accumulation is always fp64 */
+#define GS_C64 0  /* complex64 amplitudes, the reference DTYPE (statevec.py:27) */
+#define GS_C128 1 /* complex128 amplitudes, the reference with DTYPE rebound */
+
+/* lowered op kinds -- the tags of the reference op stream (pathsum.py:143-144) */
+#define GS_OP_DIAG1 0 /* ("diag1", blk, q, d2):      2 coefficients          */
+#define GS_OP_MAT1 1  /* ("mat1",  blk, q, u2):      4 coefficients, row-major */
+#define GS_OP_DIAG2 2 /* ("diag2", blk, qa, qb, d4): 4 coefficients, |qa qb>  */
+#define GS_OP_MAT2 3  /* ("mat2",  blk, qa, qb, u4): 16 coefficients, |qa qb> */
+#define GS_OP_CROSS 4 /* ("cross", k): q0 holds k; terms in the cross tables  */
+
+typedef struct gs_ctx gs_ctx;
+
+/* Run statistics; filled by gs_run when the `stats` pointer is non-NULL.
+ * Kernel times are CUDA-event durations on the context's stream and are only
+ * measured when option "profile" is 1 (events around every launch). */
+typedef struct gs_stats {
+  int64_t n_paths;           /* leaves summed (with multiplicity)           */
+  int64_t n_nodes;           /* path-tree nodes evolved, all levels          */
+  int64_t n_levels;          /* tree levels after merging (incl. root)       */
+  int64_t n_pass_launches;   /* gate-pass kernel launches                    */
+  int64_t n_gather_launches; /* gather + reduce kernel launches              */
+  int64_t n_launches;        /* every kernel launch of this run              */
+  double pass_bytes;         /* algorithmic HBM bytes of the gate passes     */
+  double gather_bytes;       /* algorithmic bytes of the gather              */
+  double ms_pass;            /* summed pass-kernel time (profile only)       */
+  double ms_gather;          /* summed gather time (profile only)            */
+  double ms_total;           /* event time of the whole gs_run               */
+  double pass_amp_updates;   /* amplitude-pass count (sum of 2^q per pass)   */
+  double pass_bytes_min;     /* one read+write per level per node (roofline) */
+  double h2d_bytes;          /* host->device bytes copied by this gs_run     */
+  double d2h_bytes;          /* device->host bytes copied by this gs_run     */
+} gs_stats;
+
+int gs_abi_version(void);
+int gs_device_count(int* out);
+
+/* Create a context on `device` (CUDA ordinal) in numeric mode GS_C64/GS_C128. */
+int gs_create(int device, int precision, gs_ctx** out);
+void gs_destroy(gs_ctx* ctx);
+const char* gs_last_error(const gs_ctx* ctx);
+
+/* Run on a caller-provided cudaStream_t (NULL: the context's own stream). */
+int gs_set_stream(gs_ctx* ctx, void* cuda_stream);
+
+/* Integer options: "mem_budget_mb" (device memory for path-tree buffers),
+ * "profile" (0/1), "tile_bits" (shared-memory tile width, 8..13),
+ * "merge_levels" (0/1: cost-model level merging), "max_chunk" (nodes/launch). */
+int gs_set_option(gs_ctx* ctx, const char* key, int64_t value);
+
+/* Load the lowered op stream of one circuit under one cut.
+ *   ops (n_ops, reference order): kind GS_OP_*, blk 0=A 1=B, q0/q1 block-local
+ *     qubit indices (q0 = k for GS_OP_CROSS), cycle of the gate, coef = offset
+ *     (in complex entries) into the coefficient pool.
+ *   cross gates (n_cross, gate order): rank, cycle, local qubit in A and in B,
+ *     and per term (sum of ranks entries, term t of gate k at
+ *     sum(rank[:k]) + t): kind (GS_OP_DIAG1 or GS_OP_MAT1) + coef offset, for
+ *     the A side and the B side (pathsum.py:160-175 term-side swap applied).
+ *   coef: n_coef complex128 values as (re, im) pairs.  In GS_C64 mode they are
+ *     rounded to complex64, as the reference's astype(DTYPE) does. */
+int gs_load_program(gs_ctx* ctx, int32_t n_qubits_a, int32_t n_qubits_b, int32_t n_ops,
+                    const int32_t* op_kind, const int32_t* op_blk, const int32_t* op_q0,
+                    const int32_t* op_q1, const int32_t* op_cycle, const int64_t* op_coef,
+                    int32_t n_cross, const int32_t* cross_rank, const int32_t* cross_cycle,
+                    const int32_t* cross_qa, const int32_t* cross_qb, const int32_t* term_kind_a,
+                    const int64_t* term_coef_a, const int32_t* term_kind_b,
+                    const int64_t* term_coef_b, int64_t n_coef, const double* coef_re_im);
+
+/* Requested amplitudes as block-local indices (split_requests, pathsum.py:122-140).
+ * Host arrays; validated against the loaded program's block sizes and uploaded. */
+int gs_set_requests(gs_ctx* ctx, int64_t n_req, const int64_t* idx_a, const int64_t* idx_b);
+
+/* Sum the contributions of the leaves {(p, b) : p in prefixes, branch_lo <= b < branch_hi}
+ * where path id = p * branch_space + b and the first x_p cross digits are the
+ * prefix (SimPlan, pathsum.py:246-274).  `prefixes` need not be sorted; each
+ * entry contributes once (duplicates count twice, like the reference loop).
+ * The complex128 result, in request order, is written to out_host (2*n_req
+ * doubles, may be NULL) and/or out_device (device pointer to 2*n_req doubles,
+ * may be NULL); with accumulate=1 it is added to out_device's contents. */
+int gs_run(gs_ctx* ctx, int32_t x_p, int64_t n_prefix, const int64_t* prefixes,
+           int64_t branch_lo, int64_t branch_hi, double* out_host, void* out_device,
+           int32_t accumulate, gs_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDSIM_B200_H */

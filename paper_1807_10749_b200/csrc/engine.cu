@@ -1,0 +1,864 @@
+// B200 path-sum engine: program loading, path-tree DFS, launches, C ABI.
+//
+// The reference executes the lowered op stream one numpy sweep per op over
+// (prefix rows x 2^q) arrays, snapshots once at the prefix/branch split and
+// replays the branch ops per branch (run_batched, pathsum.py:574-640).  Here
+// the stream is cut at every cross-gate cycle into path-tree levels; a
+// depth-first walk evolves each distinct digit prefix once, in batches of
+// sibling nodes resident in HBM, and the leaves are gathered into an fp64
+// accumulator on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/gridsim_b200.h"
+#include "kernels.cuh"
+#include "program.hpp"
+
+namespace gs {
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw GsError(GS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    release();
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      throw GsError(GS_ERR_NOMEM, "cudaMalloc(" + std::to_string(n) + ") failed: " +
+                                      cudaGetErrorString(e));
+    }
+    bytes = n;
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    CK(cudaMallocHost(&p, n));
+    bytes = n;
+  }
+};
+
+// Node of the path tree.  Leaves are (prefix index i, branch b); a node at
+// level l with digit end e covers the prefixes i0..i1-1 (all sharing digits
+// [0, min(e, x_p))) and the branch ids b0..b1-1 (all sharing digits
+// [x_p, e) when e > x_p).
+struct Node {
+  int64_t i0, i1;   // prefix index range
+  int64_t key;      // prefix digits [0, min(e, x_p)) as a number
+  int64_t bkey;     // branch digits [x_p, max(e, x_p)) as a number
+  int64_t b0, b1;   // branch id range
+  int32_t digit;    // this level's digits (mixed radix), for the cross ops
+  int32_t parent;   // slot of the parent in the previous level's buffer
+};
+
+struct Program {
+  int q[2] = {0, 0};
+  int n_cross = 0;
+  std::vector<int> radix;   // per cross gate
+  std::vector<int> cross_cycle;
+  std::vector<Level> levels;  // levels[0] = root segment (no cross digits)
+  std::vector<double> coef;   // complex pool, (re, im) pairs; cross matrices appended
+  std::vector<int32_t> xtable;
+  // per cross gate and side: xtable offset, and whether that side is diagonal
+  std::vector<int> xtab[2];
+  std::vector<int> xdiag[2];
+  std::vector<int> xq[2];
+};
+
+struct Ctx {
+  int device = -1;
+  int precision = GS_C64;
+  bool host_only = false;
+  std::string err;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  // options
+  int64_t mem_budget_mb = 0;  // 0 = auto
+  int profile = 0;
+  int tile_bits = 0;  // 0 = auto
+  int low_bits = 4;
+  int64_t max_chunk = 1 << 20;
+  // program
+  bool have_prog = false;
+  Program prog;
+  DevBuf d_ops, d_coef, d_xtable;
+  std::vector<DevOp> host_devops;
+  // requests
+  int64_t n_req = -1;
+  DevBuf d_ia, d_ib, d_acc, d_partial;
+  // tree buffers
+  std::vector<DevBuf> lvl_a, lvl_b, lvl_parent, lvl_digit;
+  std::vector<PinnedBuf> lvl_stage;
+  std::vector<cudaEvent_t> lvl_event;
+  DevBuf d_weights;
+  PinnedBuf weights_stage;
+  cudaEvent_t weights_event = nullptr;
+  // run state
+  gs_stats st{};
+  int32_t x_p = 0;
+  std::vector<int64_t> prefixes;
+  int64_t branch_lo = 0, branch_hi = 1;
+  std::vector<int64_t> S_p, S_b;  // digit suffix products
+  std::vector<int64_t> cap;        // nodes per level buffer
+  std::vector<int> lvl_end;        // digit end e_l per level
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  size_t esize() const { return precision == GS_C64 ? 8 : 16; }
+  int kmax() const {
+    int k = tile_bits ? tile_bits : (precision == GS_C64 ? 13 : 12);
+    return k;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// program loading
+
+static int64_t coef_entries(int kind) {
+  switch (kind) {
+    case K_DIAG1: return 2;
+    case K_MAT1: return 4;
+    case K_DIAG2: return 4;
+    case K_MAT2: return 16;
+  }
+  return 0;
+}
+
+static void build_program(Ctx& c, int qa, int qb, int n_ops, const int32_t* kind,
+                          const int32_t* blk, const int32_t* q0, const int32_t* q1,
+                          const int32_t* cycle, const int64_t* coef_off, int n_cross,
+                          const int32_t* rank, const int32_t* xcycle, const int32_t* xqa,
+                          const int32_t* xqb, const int32_t* tka, const int64_t* tca,
+                          const int32_t* tkb, const int64_t* tcb, int64_t n_coef,
+                          const double* coef) {
+  Program p;
+  if (qa < 1 || qb < 1 || qa > 34 || qb > 34) throw GsError(GS_ERR_ARG, "block sizes out of range");
+  p.q[0] = qa;
+  p.q[1] = qb;
+  p.coef.assign(coef, coef + 2 * n_coef);
+  p.n_cross = n_cross;
+  int64_t n_terms = 0;
+  for (int k = 0; k < n_cross; ++k) {
+    if (rank[k] < 1) throw GsError(GS_ERR_ARG, "cross rank < 1");
+    if (k > 0 && xcycle[k] < xcycle[k - 1]) throw GsError(GS_ERR_ARG, "cross gates not in cycle order");
+    p.radix.push_back(rank[k]);
+    p.cross_cycle.push_back(xcycle[k]);
+    n_terms += rank[k];
+  }
+  auto check_coef = [&](int64_t off, int64_t n) {
+    if (off < 0 || off + n > n_coef) throw GsError(GS_ERR_ARG, "coefficient offset out of range");
+  };
+  // cross tables: per side, all-diagonal terms stay diag(d0,d1); otherwise
+  // every term becomes a 2x2 (diag terms expanded), as _term_table does
+  // (pathsum.py:516-523).
+  for (int side = 0; side < 2; ++side) {
+    const int32_t* tk = side ? tkb : tka;
+    const int64_t* tc = side ? tcb : tca;
+    const int32_t* xq = side ? xqb : xqa;
+    int64_t t = 0;
+    for (int k = 0; k < n_cross; ++k) {
+      if (xq[k] < 0 || xq[k] >= p.q[side]) throw GsError(GS_ERR_ARG, "cross qubit out of block");
+      bool all_diag = true;
+      for (int d = 0; d < rank[k]; ++d) {
+        const int kk = tk[t + d];
+        if (kk != K_DIAG1 && kk != K_MAT1) throw GsError(GS_ERR_ARG, "cross term kind must be diag1/mat1");
+        all_diag &= (kk == K_DIAG1);
+      }
+      p.xtab[side].push_back((int)p.xtable.size());
+      p.xdiag[side].push_back(all_diag);
+      p.xq[side].push_back(xq[k]);
+      for (int d = 0; d < rank[k]; ++d) {
+        const int kk = tk[t + d];
+        const int64_t off = tc[t + d];
+        check_coef(off, coef_entries(kk));
+        if (all_diag || kk == K_MAT1) {
+          p.xtable.push_back((int32_t)off);
+        } else {  // expand diag(d0, d1) to a 2x2 in the pool
+          const int64_t at = (int64_t)p.coef.size() / 2;
+          const double m[8] = {coef[2 * off], coef[2 * off + 1], 0, 0, 0, 0,
+                               coef[2 * off + 2], coef[2 * off + 3]};
+          p.coef.insert(p.coef.end(), m, m + 8);
+          p.xtable.push_back((int32_t)at);
+        }
+      }
+      t += rank[k];
+    }
+  }
+  if ((int64_t)p.coef.size() / 2 > INT32_MAX) throw GsError(GS_ERR_ARG, "coefficient pool too large");
+
+  // levels: distinct cross cycles; level l (>= 1) starts at cross cycle c_l
+  std::vector<int> lvl_cycle;
+  std::vector<int> lvl_klo;
+  for (int k = 0; k < n_cross; ++k)
+    if (k == 0 || xcycle[k] != xcycle[k - 1]) lvl_cycle.push_back(xcycle[k]), lvl_klo.push_back(k);
+  const int D = (int)lvl_cycle.size();
+  p.levels.resize(D + 1);
+  for (int l = 1; l <= D; ++l) {
+    p.levels[l].k_lo = lvl_klo[l - 1];
+    p.levels[l].k_hi = (l < D) ? lvl_klo[l] : n_cross;
+    // cross ops first: every op of a cycle acts on disjoint qubits, so the
+    // cycle's cross terms commute with its other ops
+    for (int k = p.levels[l].k_lo; k < p.levels[l].k_hi; ++k)
+      for (int side = 0; side < 2; ++side) {
+        HostOp op;
+        op.kind = p.xdiag[side][k] ? K_DIAG1 : K_MAT1;
+        op.s0 = p.q[side] - 1 - p.xq[side][k];
+        op.cross = k;
+        p.levels[l].ops[side].push_back(op);
+      }
+  }
+  int seen_cross = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    const int kd = kind[i];
+    if (kd == K_CROSS) {
+      if (q0[i] != seen_cross) throw GsError(GS_ERR_ARG, "cross ops out of order");
+      ++seen_cross;
+      continue;
+    }
+    if (kd < 0 || kd > K_MAT2) throw GsError(GS_ERR_ARG, "unknown op kind");
+    const int side = blk[i];
+    if (side != 0 && side != 1) throw GsError(GS_ERR_ARG, "op block must be 0 or 1");
+    const int q = p.q[side];
+    HostOp op;
+    op.kind = kd;
+    if (q0[i] < 0 || q0[i] >= q) throw GsError(GS_ERR_ARG, "op qubit out of block");
+    op.s0 = q - 1 - q0[i];
+    if (kd == K_DIAG2 || kd == K_MAT2) {
+      if (q1[i] < 0 || q1[i] >= q || q1[i] == q0[i]) throw GsError(GS_ERR_ARG, "bad second qubit");
+      op.s1 = q - 1 - q1[i];
+    }
+    op.coef = coef_off[i];
+    check_coef(op.coef, coef_entries(kd));
+    // level = number of cross cycles <= this op's cycle
+    const int l = (int)(std::upper_bound(lvl_cycle.begin(), lvl_cycle.end(), cycle[i]) - lvl_cycle.begin());
+    p.levels[l].ops[side].push_back(op);
+  }
+  if (seen_cross != n_cross) throw GsError(GS_ERR_ARG, "cross op count mismatch");
+  c.prog = std::move(p);
+}
+
+static void schedule_program(Ctx& c) {
+  Program& p = c.prog;
+  c.host_devops.clear();
+  for (size_t l = 0; l < p.levels.size(); ++l) {
+    Level& L = p.levels[l];
+    for (int side = 0; side < 2; ++side) {
+      L.passes[side] = schedule_passes(L.ops[side], p.q[side], c.kmax(), c.low_bits, true);
+      for (PassPlan& pp : L.passes[side]) {
+        pp.dev_op_offset = (int64_t)c.host_devops.size();
+        std::vector<int> tpos(p.q[side], -1);
+        for (int j = 0; j < (int)pp.lbits.size(); ++j) tpos[pp.lbits[j]] = j;
+        for (const HostOp& op : pp.ops) {
+          DevOp d{};
+          d.xtab = -1;
+          d.xstride = 1;
+          d.xradix = 1;
+          d.coef = (int32_t)op.coef;
+          if (op.cross >= 0) {
+            d.xtab = p.xtab[side][op.cross];
+            int64_t stride = 1;
+            for (int k = op.cross + 1; k < L.k_hi; ++k) stride *= p.radix[k];
+            d.xstride = (int32_t)stride;
+            d.xradix = p.radix[op.cross];
+          }
+          auto enc = [&](int s, int32_t& b, int32_t& g) {
+            if (s < 0) { b = 0; g = 0; return; }
+            if (tpos[s] >= 0) { b = tpos[s]; g = 0; } else { b = s; g = 1; }
+          };
+          enc(op.s0, d.b0, d.g0);
+          enc(op.s1, d.b1, d.g1);
+          switch (op.kind) {
+            case K_MAT1: d.type = D_MAT1; break;
+            case K_DIAG1: d.type = D_DIAG1; break;
+            case K_DIAG2: d.type = D_DIAG2; break;
+            default: d.type = D_MAT2; break;
+          }
+          if ((d.type == D_MAT1 || d.type == D_MAT2) && (d.g0 || d.g1))
+            throw GsError(GS_ERR_ARG, "scheduler placed a dense op outside the tile");
+          c.host_devops.push_back(d);
+        }
+      }
+    }
+  }
+  // level digit products must fit int32 node digits
+  for (size_t l = 1; l < p.levels.size(); ++l) {
+    int64_t f = 1;
+    for (int k = p.levels[l].k_lo; k < p.levels[l].k_hi; ++k) {
+      f *= p.radix[k];
+      if (f > INT32_MAX) throw GsError(GS_ERR_ARG, "level fan-out exceeds int32");
+    }
+  }
+}
+
+template <typename T> static void upload(Ctx& c, DevBuf& b, const std::vector<T>& v) {
+  b.ensure(std::max<size_t>(v.size() * sizeof(T), 16));
+  if (!v.empty()) CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+static void upload_program(Ctx& c) {
+  if (c.host_only) return;
+  upload(c, c.d_ops, c.host_devops);
+  upload(c, c.d_xtable, c.prog.xtable);
+  if (c.precision == GS_C64) {
+    std::vector<float> f(c.prog.coef.begin(), c.prog.coef.end());
+    upload(c, c.d_coef, f);
+  } else {
+    upload(c, c.d_coef, c.prog.coef);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tree enumeration
+
+static int64_t level_fanout(const Program& p, int l) {
+  int64_t f = 1;
+  for (int k = p.levels[l].k_lo; k < p.levels[l].k_hi; ++k) f *= p.radix[k];
+  return f;
+}
+
+// children of `parents` (level l) at level l+1, appended to `out` in leaf order
+static void enumerate_children(Ctx& c, int l, const Node* parents, int64_t n_par,
+                               std::vector<Node>& out) {
+  const Program& p = c.prog;
+  const int e0 = c.lvl_end[l], e1 = c.lvl_end[l + 1];
+  const int xp = c.x_p;
+  const std::vector<int64_t>& pre = c.prefixes;
+  for (int64_t s = 0; s < n_par; ++s) {
+    const Node& N = parents[s];
+    if (e1 <= xp) {
+      const int64_t S = c.S_p[e1];
+      const int64_t F = level_fanout(p, l + 1);
+      int64_t i = N.i0;
+      while (i < N.i1) {
+        const int64_t ck = pre[i] / S;
+        const int64_t lim = (ck + 1) * S;  // first prefix value of the next child
+        const int64_t j = std::lower_bound(pre.begin() + i, pre.begin() + N.i1, lim) - pre.begin();
+        Node ch{i, j, ck, 0, N.b0, N.b1, (int32_t)(ck - N.key * F), (int32_t)s};
+        out.push_back(ch);
+        i = j;
+      }
+    } else {
+      const int kb0 = std::max(e0, xp);
+      int64_t Fb = 1;
+      for (int k = kb0; k < e1; ++k) Fb *= p.radix[k];
+      const int64_t Sb = c.S_b[e1];
+      int64_t lo = std::max(N.bkey * Fb, N.b0 / Sb);
+      int64_t hi = std::min((N.bkey + 1) * Fb - 1, (N.b1 - 1) / Sb);
+      for (int64_t i = N.i0; i < N.i1; ++i) {
+        const int64_t vp = (e0 < xp) ? (pre[i] % c.S_p[e0]) : 0;
+        for (int64_t cb = lo; cb <= hi; ++cb) {
+          const int64_t b0 = std::max(cb * Sb, N.b0), b1 = std::min((cb + 1) * Sb, N.b1);
+          if (b0 >= b1) continue;
+          Node ch{i, i + 1, pre[i], cb, b0, b1, (int32_t)(vp * Fb + (cb - N.bkey * Fb)), (int32_t)s};
+          out.push_back(ch);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launches
+
+template <typename R>
+static void launch_pass(Ctx& c, int side, const PassPlan& pp, const void* src, void* dst,
+                        const int32_t* parent, const int32_t* digit, int64_t n_states,
+                        bool init_zero) {
+  const int q = c.prog.q[side];
+  PassArgs a{};
+  a.src = src;
+  a.dst = dst;
+  a.parent = parent;
+  a.digit = digit;
+  a.ops = reinterpret_cast<const DevOp*>(c.d_ops.p) + pp.dev_op_offset;
+  a.coefs = c.d_coef.p;
+  a.xtable = reinterpret_cast<const int32_t*>(c.d_xtable.p);
+  a.state_elems = 1LL << q;
+  a.n_ops = (int)pp.ops.size();
+  a.k = pp.k;
+  int cc = 0;
+  while (cc < pp.k && pp.lbits[cc] == cc) ++cc;
+  a.c = std::min(cc, 8);
+  a.tiles_log = q - pp.k;
+  a.init_zero = init_zero ? 1 : 0;
+  a.n_hi = 1 << (pp.k - a.c);
+  for (int j = 0; j < pp.k; ++j) a.lbits[j] = pp.lbits[j];
+  for (int j = 0; j < (int)pp.gbits.size(); ++j) a.gbits[j] = pp.gbits[j];
+  const int E = 1 << pp.k;
+  const int threads = std::max(32, std::min(256, E / 2));
+  const size_t smem = (size_t)E * c.esize() + (size_t)a.n_hi * sizeof(int);
+  const int64_t blocks = n_states << a.tiles_log;
+  if (blocks > INT32_MAX) throw GsError(GS_ERR_ARG, "grid too large");
+  c.st.n_pass_launches++;
+  c.st.n_launches++;
+  c.st.pass_bytes += 2.0 * (double)n_states * (double)(1LL << q) * (double)c.esize();
+  c.st.pass_amp_updates += (double)n_states * (double)(1LL << q);
+  if (c.host_only) return;
+  gate_pass_kernel<R><<<(unsigned)blocks, threads, smem, c.stream>>>(a);
+  CK(cudaGetLastError());
+}
+
+struct Timer {
+  Ctx& c;
+  double* acc;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timer(Ctx& cc, double* ac) : c(cc), acc(ac) {
+    if (c.profile && !c.host_only) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, c.stream);
+    }
+  }
+  ~Timer() {
+    if (a) {
+      cudaEventRecord(b, c.stream);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      *acc += ms;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  }
+};
+
+template <typename R>
+static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const void* src_b,
+                             void* dst_a, void* dst_b, const int32_t* parent,
+                             const int32_t* digit, bool root) {
+  Timer t(c, &c.st.ms_pass);
+  const Level& L = c.prog.levels[l];
+  const void* srcs[2] = {src_a, src_b};
+  void* dsts[2] = {dst_a, dst_b};
+  for (int side = 0; side < 2; ++side) {
+    bool first = true;
+    for (const PassPlan& pp : L.passes[side]) {
+      launch_pass<R>(c, side, pp, first ? srcs[side] : dsts[side], dsts[side],
+                     first ? parent : nullptr, digit, n, root && first);
+      first = false;
+    }
+  }
+  c.st.n_nodes += n;
+  for (int side = 0; side < 2; ++side)
+    c.st.pass_bytes_min += 2.0 * (double)n * (double)(1LL << c.prog.q[side]) * (double)c.esize();
+}
+
+template <typename R> static void gather(Ctx& c, int l, const std::vector<Node>& nodes) {
+  const int64_t n = (int64_t)nodes.size();
+  // leaf multiplicity: duplicate prefixes / branch ranges collapsed into one node
+  int64_t w_total = 0;
+  for (int64_t j = 0; j < n; ++j) w_total += (nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0);
+  c.st.n_paths += w_total;
+  if (c.host_only || c.n_req == 0) return;
+  c.weights_stage.ensure(n * sizeof(double));
+  cudaEventSynchronize(c.weights_event);
+  double* w = reinterpret_cast<double*>(c.weights_stage.p);
+  for (int64_t j = 0; j < n; ++j) w[j] = (double)((nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0));
+  Timer t(c, &c.st.ms_gather);
+  c.d_weights.ensure(std::max<size_t>(n * sizeof(double), 16));
+  CK(cudaMemcpyAsync(c.d_weights.p, w, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  c.st.h2d_bytes += 8.0 * n;
+  CK(cudaEventRecord(c.weights_event, c.stream));
+  const int64_t nreq = c.n_req;
+  const int threads = 256;
+  const int64_t xblocks = (nreq + threads - 1) / threads;
+  // enough leaf groups to fill the GPU, bounded by the partial buffer
+  int64_t groups = std::max<int64_t>(1, (148 * 16) / std::max<int64_t>(1, xblocks));
+  groups = std::min<int64_t>(groups, n);
+  const int64_t max_groups = std::max<int64_t>(1, (256LL << 20) / (16 * std::max<int64_t>(1, nreq)));
+  groups = std::min(groups, max_groups);
+  groups = std::min<int64_t>(groups, 65535);
+  const int64_t per = (n + groups - 1) / groups;
+  groups = (n + per - 1) / per;
+  c.d_partial.ensure((size_t)groups * nreq * sizeof(double2));
+  const int qa = c.prog.q[0], qb = c.prog.q[1];
+  dim3 grid((unsigned)xblocks, (unsigned)groups);
+  gather_kernel<R><<<grid, threads, 0, c.stream>>>(
+      c.lvl_a[l].p, c.lvl_b[l].p, 1LL << qa, 1LL << qb, (int)n, (int)per,
+      reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const int32_t*>(c.d_ia.p),
+      reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
+  CK(cudaGetLastError());
+  reduce_kernel<<<(unsigned)xblocks, threads, 0, c.stream>>>(
+      reinterpret_cast<const double2*>(c.d_partial.p), (int)groups, nreq,
+      reinterpret_cast<double2*>(c.d_acc.p));
+  CK(cudaGetLastError());
+  c.st.n_gather_launches += 2;
+  c.st.n_launches += 2;
+  c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
+}
+
+template <typename R> static void descend(Ctx& c, int l, const std::vector<Node>& nodes) {
+  const int D = (int)c.prog.levels.size() - 1;
+  if (l == D) {
+    gather<R>(c, l, nodes);
+    return;
+  }
+  std::vector<Node> kids;
+  enumerate_children(c, l, nodes.data(), (int64_t)nodes.size(), kids);
+  const int64_t cap = c.cap[l + 1];
+  const size_t ea = (size_t)(1LL << c.prog.q[0]), eb = (size_t)(1LL << c.prog.q[1]);
+  for (int64_t s = 0; s < (int64_t)kids.size(); s += cap) {
+    const int64_t n = std::min<int64_t>(cap, (int64_t)kids.size() - s);
+    std::vector<Node> chunk(kids.begin() + s, kids.begin() + s + n);
+    if (!c.host_only) {
+      PinnedBuf& stg = c.lvl_stage[l + 1];
+      cudaEventSynchronize(c.lvl_event[l + 1]);
+      int32_t* h = reinterpret_cast<int32_t*>(stg.p);
+      for (int64_t j = 0; j < n; ++j) h[j] = chunk[j].parent, h[n + j] = chunk[j].digit;
+      CK(cudaMemcpyAsync(c.lvl_parent[l + 1].p, h, n * 4, cudaMemcpyHostToDevice, c.stream));
+      CK(cudaMemcpyAsync(c.lvl_digit[l + 1].p, h + n, n * 4, cudaMemcpyHostToDevice, c.stream));
+      c.st.h2d_bytes += 8.0 * n;
+      CK(cudaEventRecord(c.lvl_event[l + 1], c.stream));
+    }
+    auto at = [](std::vector<DevBuf>& v, int i) -> void* { return i < (int)v.size() ? v[i].p : nullptr; };
+    run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
+                        at(c.lvl_b, l + 1), reinterpret_cast<const int32_t*>(at(c.lvl_parent, l + 1)),
+                        reinterpret_cast<const int32_t*>(at(c.lvl_digit, l + 1)), false);
+    (void)ea;
+    (void)eb;
+    descend<R>(c, l + 1, chunk);
+  }
+}
+
+static void plan_buffers(Ctx& c, int64_t n_leaves) {
+  const Program& p = c.prog;
+  const int D = (int)p.levels.size() - 1;
+  const double pair = (double)((1LL << p.q[0]) + (1LL << p.q[1])) * (double)c.esize();
+  // upper bound on nodes per level
+  std::vector<double> bound(D + 1, 1.0);
+  double prod = 1.0;
+  for (int l = 1; l <= D; ++l) {
+    prod *= (double)level_fanout(p, l);
+    bound[l] = std::min(prod, (double)n_leaves);
+  }
+  double budget;
+  if (c.mem_budget_mb > 0) {
+    budget = (double)c.mem_budget_mb * 1048576.0;
+  } else if (c.host_only) {
+    budget = 64e9;
+  } else {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    budget = 0.80 * (double)fr - 1.5e9;
+    budget = std::max(budget, 4.0 * pair);
+  }
+  // largest uniform cap with sum_l min(bound_l, cap) * pair <= budget
+  auto need = [&](double cap) {
+    double s = 0;
+    for (int l = 0; l <= D; ++l) s += std::min(bound[l], cap) * pair;
+    return s;
+  };
+  double lo = 1, hi = (double)c.max_chunk;
+  if (need(1) > budget) throw GsError(GS_ERR_NOMEM, "device memory budget below one node per level");
+  while (hi - lo > 0.5) {
+    double mid = std::floor((lo + hi + 1) / 2);
+    if (need(mid) <= budget) lo = mid; else hi = mid - 1;
+  }
+  c.cap.assign(D + 1, 1);
+  for (int l = 0; l <= D; ++l) c.cap[l] = (int64_t)std::max(1.0, std::min(bound[l], lo));
+  if (c.host_only) return;
+  c.lvl_a.resize(D + 1);
+  c.lvl_b.resize(D + 1);
+  c.lvl_parent.resize(D + 1);
+  c.lvl_digit.resize(D + 1);
+  c.lvl_stage.resize(D + 1);
+  while ((int)c.lvl_event.size() < D + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.lvl_event.push_back(e);
+  }
+  for (int l = 0; l <= D; ++l) {
+    c.lvl_a[l].ensure((size_t)c.cap[l] * ((size_t)1 << p.q[0]) * c.esize());
+    c.lvl_b[l].ensure((size_t)c.cap[l] * ((size_t)1 << p.q[1]) * c.esize());
+    c.lvl_parent[l].ensure(c.cap[l] * 4 + 16);
+    c.lvl_digit[l].ensure(c.cap[l] * 4 + 16);
+    c.lvl_stage[l].ensure(c.cap[l] * 8 + 16);
+  }
+  if (!c.weights_event) CK(cudaEventCreateWithFlags(&c.weights_event, cudaEventDisableTiming));
+}
+
+template <typename R>
+static void run_tree(Ctx& c) {
+  const Program& p = c.prog;
+  const int D = (int)p.levels.size() - 1;
+  int64_t n_leaves_bound = (int64_t)c.prefixes.size() * (c.branch_hi - c.branch_lo);
+  plan_buffers(c, std::max<int64_t>(1, n_leaves_bound));
+  c.st.n_levels = D + 1;
+  // root: |0...0> through the root segment
+  run_level_passes<R>(c, 0, 1, nullptr, nullptr, c.lvl_a.empty() ? nullptr : c.lvl_a[0].p,
+                      c.lvl_b.empty() ? nullptr : c.lvl_b[0].p, nullptr, nullptr, true);
+  std::vector<Node> root{{0, (int64_t)c.prefixes.size(), 0, 0, c.branch_lo, c.branch_hi, 0, 0}};
+  if (c.prefixes.empty() || c.branch_hi <= c.branch_lo) return;
+  descend<R>(c, 0, root);
+}
+
+}  // namespace gs
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+using gs::Ctx;
+using gs::GsError;
+
+struct gs_ctx {
+  Ctx c;
+};
+
+#define GS_GUARD(ctx, ...)                                   \
+  do {                                                       \
+    try {                                                    \
+      __VA_ARGS__;                                           \
+      return GS_OK;                                          \
+    } catch (const GsError& e) {                             \
+      if (ctx) (ctx)->c.err = e.what();                      \
+      return e.code;                                         \
+    } catch (const std::bad_alloc&) {                        \
+      if (ctx) (ctx)->c.err = "host out of memory";          \
+      return GS_ERR_NOMEM;                                   \
+    } catch (const std::exception& e) {                      \
+      if (ctx) (ctx)->c.err = e.what();                      \
+      return GS_ERR_ARG;                                     \
+    }                                                        \
+  } while (0)
+
+extern "C" {
+
+int gs_abi_version(void) { return GS_ABI_VERSION; }
+
+int gs_device_count(int* out) {
+  if (!out) return GS_ERR_ARG;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *out = 0;
+    return GS_OK;
+  }
+  *out = n;
+  return GS_OK;
+}
+
+int gs_create(int device, int precision, gs_ctx** out) {
+  if (!out) return GS_ERR_ARG;
+  *out = nullptr;
+  if (precision != GS_C64 && precision != GS_C128) return GS_ERR_ARG;
+  gs_ctx* h = new (std::nothrow) gs_ctx();
+  if (!h) return GS_ERR_NOMEM;
+  h->c.precision = precision;
+  h->c.device = device;
+  if (device < 0) {
+    h->c.host_only = true;  // planning / dry runs only (CPU tests)
+    *out = h;
+    return GS_OK;
+  }
+  try {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&h->c.own_stream, cudaStreamNonBlocking));
+    h->c.stream = h->c.own_stream;
+    CK(cudaEventCreate(&h->c.ev0));
+    CK(cudaEventCreate(&h->c.ev1));
+    CK(cudaFuncSetAttribute(gs::gate_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(gs::gate_pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  } catch (const GsError& e) {
+    std::fprintf(stderr, "gs_create: %s\n", e.what());
+    delete h;
+    return e.code;
+  }
+  *out = h;
+  return GS_OK;
+}
+
+void gs_destroy(gs_ctx* ctx) {
+  if (!ctx) return;
+  if (!ctx->c.host_only) {
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    for (auto e : ctx->c.lvl_event) cudaEventDestroy(e);
+    if (ctx->c.weights_event) cudaEventDestroy(ctx->c.weights_event);
+    if (ctx->c.ev0) cudaEventDestroy(ctx->c.ev0);
+    if (ctx->c.ev1) cudaEventDestroy(ctx->c.ev1);
+    if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
+  }
+  delete ctx;
+}
+
+const char* gs_last_error(const gs_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
+
+int gs_set_stream(gs_ctx* ctx, void* s) {
+  if (!ctx) return GS_ERR_ARG;
+  ctx->c.stream = s ? reinterpret_cast<cudaStream_t>(s) : ctx->c.own_stream;
+  return GS_OK;
+}
+
+int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
+  if (!ctx || !key) return GS_ERR_ARG;
+  GS_GUARD(ctx, {
+    std::string k(key);
+    Ctx& c = ctx->c;
+    if (k == "mem_budget_mb") c.mem_budget_mb = value;
+    else if (k == "profile") c.profile = (int)value;
+    else if (k == "tile_bits") {
+      if (value != 0 && (value < 4 || value > (c.precision == GS_C64 ? 14 : 13)))
+        throw GsError(GS_ERR_ARG, "tile_bits out of range");
+      c.tile_bits = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "low_bits") {
+      if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "low_bits out of range");
+      c.low_bits = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "max_chunk") {
+      if (value < 1) throw GsError(GS_ERR_ARG, "max_chunk must be positive");
+      c.max_chunk = value;
+    } else throw GsError(GS_ERR_ARG, "unknown option " + k);
+  });
+}
+
+int gs_load_program(gs_ctx* ctx, int32_t qa, int32_t qb, int32_t n_ops, const int32_t* op_kind,
+                    const int32_t* op_blk, const int32_t* op_q0, const int32_t* op_q1,
+                    const int32_t* op_cycle, const int64_t* op_coef, int32_t n_cross,
+                    const int32_t* cross_rank, const int32_t* cross_cycle, const int32_t* cross_qa,
+                    const int32_t* cross_qb, const int32_t* term_kind_a, const int64_t* term_coef_a,
+                    const int32_t* term_kind_b, const int64_t* term_coef_b, int64_t n_coef,
+                    const double* coef) {
+  if (!ctx) return GS_ERR_ARG;
+  GS_GUARD(ctx, {
+    Ctx& c = ctx->c;
+    if (n_ops < 0 || n_cross < 0 || n_coef < 0) throw GsError(GS_ERR_ARG, "negative count");
+    if (n_ops > 0 && (!op_kind || !op_blk || !op_q0 || !op_q1 || !op_cycle || !op_coef))
+      throw GsError(GS_ERR_ARG, "null op array");
+    if (n_cross > 0 && (!cross_rank || !cross_cycle || !cross_qa || !cross_qb || !term_kind_a ||
+                        !term_coef_a || !term_kind_b || !term_coef_b))
+      throw GsError(GS_ERR_ARG, "null cross array");
+    if (!c.host_only) CK(cudaSetDevice(c.device));
+    c.have_prog = false;
+    gs::build_program(c, qa, qb, n_ops, op_kind, op_blk, op_q0, op_q1, op_cycle, op_coef, n_cross,
+                      cross_rank, cross_cycle, cross_qa, cross_qb, term_kind_a, term_coef_a,
+                      term_kind_b, term_coef_b, n_coef, coef);
+    gs::schedule_program(c);
+    gs::upload_program(c);
+    c.have_prog = true;
+    c.n_req = -1;
+  });
+}
+
+int gs_set_requests(gs_ctx* ctx, int64_t n_req, const int64_t* ia, const int64_t* ib) {
+  if (!ctx) return GS_ERR_ARG;
+  GS_GUARD(ctx, {
+    Ctx& c = ctx->c;
+    if (!c.have_prog) throw GsError(GS_ERR_STATE, "no program loaded");
+    if (n_req < 0 || (n_req > 0 && (!ia || !ib))) throw GsError(GS_ERR_ARG, "bad request arrays");
+    const int64_t na = 1LL << c.prog.q[0], nb = 1LL << c.prog.q[1];
+    std::vector<int32_t> a(n_req), b(n_req);
+    for (int64_t i = 0; i < n_req; ++i) {
+      if (ia[i] < 0 || ia[i] >= na || ib[i] < 0 || ib[i] >= nb)
+        throw GsError(GS_ERR_INDEX, "request index outside the state space");
+      a[i] = (int32_t)ia[i];
+      b[i] = (int32_t)ib[i];
+    }
+    if (!c.host_only) {
+      CK(cudaSetDevice(c.device));
+      gs::upload(c, c.d_ia, a);
+      gs::upload(c, c.d_ib, b);
+      c.d_acc.ensure(std::max<size_t>(n_req * sizeof(double2), 16));
+    }
+    c.n_req = n_req;
+  });
+}
+
+int gs_run(gs_ctx* ctx, int32_t x_p, int64_t n_prefix, const int64_t* prefixes, int64_t branch_lo,
+           int64_t branch_hi, double* out_host, void* out_device, int32_t accumulate,
+           gs_stats* stats) {
+  if (!ctx) return GS_ERR_ARG;
+  GS_GUARD(ctx, {
+    Ctx& c = ctx->c;
+    if (!c.have_prog) throw GsError(GS_ERR_STATE, "no program loaded");
+    if (c.n_req < 0) throw GsError(GS_ERR_STATE, "no requests loaded");
+    const gs::Program& p = c.prog;
+    const int x = p.n_cross;
+    if (x_p < 0 || x_p > x) throw GsError(GS_ERR_PLAN, "x_p outside [0, x]");
+    if (n_prefix < 0 || (n_prefix > 0 && !prefixes)) throw GsError(GS_ERR_ARG, "bad prefix array");
+    // digit suffix products; spaces must fit int64
+    c.x_p = x_p;
+    c.S_p.assign(x_p + 1, 1);
+    for (int k = x_p - 1; k >= 0; --k) {
+      if (c.S_p[k + 1] > (INT64_MAX / 8) / p.radix[k]) throw GsError(GS_ERR_ARG, "prefix space exceeds int64");
+      c.S_p[k] = c.S_p[k + 1] * p.radix[k];
+    }
+    c.S_b.assign(x + 1, 1);
+    for (int k = x - 1; k >= x_p; --k) {
+      if (c.S_b[k + 1] > (INT64_MAX / 8) / p.radix[k]) throw GsError(GS_ERR_ARG, "branch space exceeds int64");
+      c.S_b[k] = c.S_b[k + 1] * p.radix[k];
+    }
+    const int64_t prefix_space = c.S_p[0], branch_space = c.S_b[x_p];
+    if (branch_lo < 0 || branch_hi > branch_space || branch_lo > branch_hi)
+      throw GsError(GS_ERR_ARG, "branch range outside the branch space");
+    c.prefixes.assign(prefixes, prefixes + n_prefix);
+    for (int64_t v : c.prefixes)
+      if (v < 0 || v >= prefix_space) throw GsError(GS_ERR_ARG, "prefix id outside the prefix space");
+    std::sort(c.prefixes.begin(), c.prefixes.end());
+    c.branch_lo = branch_lo;
+    c.branch_hi = branch_hi;
+    c.lvl_end.assign(p.levels.size(), 0);
+    for (size_t l = 1; l < p.levels.size(); ++l) c.lvl_end[l] = p.levels[l].k_hi;
+    c.st = gs_stats{};
+    if (!c.host_only) {
+      CK(cudaSetDevice(c.device));
+      if (!accumulate || !out_device) {
+        CK(cudaMemsetAsync(c.d_acc.p, 0, std::max<size_t>(c.n_req * sizeof(double2), 16), c.stream));
+      } else {
+        CK(cudaMemcpyAsync(c.d_acc.p, out_device, c.n_req * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream));
+      }
+      CK(cudaEventRecord(c.ev0, c.stream));
+    }
+    if (c.precision == GS_C64) gs::run_tree<float>(c);
+    else gs::run_tree<double>(c);
+    if (!c.host_only) {
+      CK(cudaEventRecord(c.ev1, c.stream));
+      if (out_device && c.n_req > 0)
+        CK(cudaMemcpyAsync(out_device, c.d_acc.p, c.n_req * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream));
+      if (out_host && c.n_req > 0) {
+        CK(cudaMemcpyAsync(out_host, c.d_acc.p, c.n_req * sizeof(double2), cudaMemcpyDeviceToHost, c.stream));
+        c.st.d2h_bytes += 16.0 * c.n_req;
+      }
+      CK(cudaStreamSynchronize(c.stream));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+      c.st.ms_total = ms;
+    } else if (out_host) {
+      std::fill(out_host, out_host + 2 * std::max<int64_t>(c.n_req, 0), 0.0);
+    }
+    if (stats) *stats = c.st;
+  });
+}
+
+}  // extern "C"

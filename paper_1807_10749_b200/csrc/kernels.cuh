@@ -1,0 +1,222 @@
+// Device kernels of the path-sum engine (sm_100a).
+//
+// gate_pass_kernel   one fused pass of lowered ops over a batch of half-states
+//                    (replaces one numpy sweep per op in _exec_ops_batched,
+//                    pathsum.py:537-557, and the _b_* kernels :450-513).
+// gather_kernel      per-request amplitude gather + fp64 multiply-accumulate
+//                    over a batch of leaf states (`land`, pathsum.py:607-615).
+// reduce_kernel      deterministic fold of the gather partials into the
+//                    complex128 accumulator (fixed order, no atomics).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gs {
+
+// ---------------------------------------------------------------------------
+// device op encoding (built on the host by the pass scheduler)
+
+enum DevOpType : int32_t {
+  D_MAT1 = 0,  // dense 2x2 on tile bit b0
+  D_DIAG1 = 1, // diag(d0,d1) on bit b0 (tile bit, or state bit if g0)
+  D_DIAG2 = 2, // diag(d00,d01,d10,d11) on bits (b0,b1) each tile/state
+  D_MAT2 = 3,  // dense 4x4 on tile bits (b0 = qa, b1 = qb), |qa qb> order
+};
+
+struct DevOp {
+  int32_t type;
+  int32_t b0, b1;  // tile bit (g*=0) or state bit (g*=1)
+  int32_t g0, g1;  // 1 = bit is outside the tile (fixed per tile)
+  int32_t coef;    // coefficient offset (non-cross ops)
+  int32_t xtab;    // >= 0: cross op; coef = xtable[xtab + digit]
+  int32_t xstride; // digit = (node_digit / xstride) % xradix
+  int32_t xradix;
+  int32_t pad;
+};
+
+template <typename R> struct Cx;
+template <> struct Cx<float> { using T = float2; };
+template <> struct Cx<double> { using T = double2; };
+
+template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
+  V r;
+  r.x = a.x * b.x - a.y * b.y;
+  r.y = a.x * b.y + a.y * b.x;
+  return r;
+}
+template <typename V> __device__ __forceinline__ V cmad2(V u0, V a, V u1, V b) {
+  // u0*a + u1*b, complex
+  V r;
+  r.x = u0.x * a.x - u0.y * a.y + u1.x * b.x - u1.y * b.y;
+  r.y = u0.x * a.y + u0.y * a.x + u1.x * b.y + u1.y * b.x;
+  return r;
+}
+
+struct PassArgs {
+  const void* src;         // parent states (first pass) or dst (in place)
+  void* dst;               // child states
+  const int32_t* parent;   // parent slot per child state, nullptr = identity
+  const int32_t* digit;    // node digit per child state (cross ops), may be null
+  const DevOp* ops;
+  const void* coefs;
+  const int32_t* xtable;
+  long long state_elems;   // 2^q
+  int n_ops;
+  int k;                   // tile bits
+  int c;                   // low state bits always in the tile (contiguous run)
+  int tiles_log;           // q - k
+  int init_zero;           // root pass: tile starts as |0...0>
+  int n_hi;                // 2^(k-c) entries of hi_off
+  int lbits[16];           // tile bit j -> state bit
+  int gbits[32];           // tile-id bit j -> state bit
+};
+
+template <typename R>
+__global__ void __launch_bounds__(256) gate_pass_kernel(PassArgs a) {
+  using V = typename Cx<R>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* tile = reinterpret_cast<V*>(smem_raw);
+  const int E = 1 << a.k;
+  int* hi_off = reinterpret_cast<int*>(tile + E);
+  const int tid = threadIdx.x;
+  const int nt = blockDim.x;
+
+  const long long state = (long long)(blockIdx.x >> a.tiles_log);
+  const int tile_id = blockIdx.x & ((1 << a.tiles_log) - 1);
+  long long base = 0;
+  for (int j = 0; j < a.tiles_log; ++j) base |= (long long)((tile_id >> j) & 1) << a.gbits[j];
+  // offsets of the strided (non-contiguous) tile bits
+  for (int h = tid; h < a.n_hi; h += nt) {
+    int off = 0;
+    for (int j = a.c; j < a.k; ++j) off |= ((h >> (j - a.c)) & 1) << a.lbits[j];
+    hi_off[h] = off;
+  }
+  __syncthreads();
+  const int cmask = (1 << a.c) - 1;
+
+  const V* src = reinterpret_cast<const V*>(a.src);
+  V* dst = reinterpret_cast<V*>(a.dst);
+  const long long src_state = a.parent ? (long long)a.parent[state] : state;
+  if (a.init_zero) {
+    for (int t = tid; t < E; t += nt) {
+      long long off = base | (t & cmask) | hi_off[t >> a.c];
+      V v;
+      v.x = (off == 0) ? R(1) : R(0);
+      v.y = R(0);
+      tile[t] = v;
+    }
+  } else {
+    const V* s = src + src_state * a.state_elems + base;
+    for (int t = tid; t < E; t += nt) tile[t] = s[(t & cmask) | hi_off[t >> a.c]];
+  }
+  __syncthreads();
+
+  const V* coefs = reinterpret_cast<const V*>(a.coefs);
+  const int node_digit = a.digit ? a.digit[state] : 0;
+  for (int oi = 0; oi < a.n_ops; ++oi) {
+    const DevOp op = a.ops[oi];
+    int cofs = op.coef;
+    if (op.xtab >= 0) cofs = a.xtable[op.xtab + (node_digit / op.xstride) % op.xradix];
+    const V* u = coefs + cofs;
+    if (op.type == D_MAT1) {
+      const V u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+      const int j = op.b0;
+      const int lo = (1 << j) - 1;
+      for (int p = tid; p < (E >> 1); p += nt) {
+        const int t0 = ((p & ~lo) << 1) | (p & lo);
+        const int t1 = t0 | (1 << j);
+        const V v0 = tile[t0], v1 = tile[t1];
+        tile[t0] = cmad2(u00, v0, u01, v1);
+        tile[t1] = cmad2(u10, v0, u11, v1);
+      }
+    } else if (op.type == D_DIAG1) {
+      const V d0 = u[0], d1 = u[1];
+      if (op.g0) {
+        const V d = ((base >> op.b0) & 1) ? d1 : d0;
+        if (!(d.x == R(1) && d.y == R(0)))
+          for (int t = tid; t < E; t += nt) tile[t] = cmul(tile[t], d);
+      } else {
+        const int j = op.b0;
+        for (int t = tid; t < E; t += nt) tile[t] = cmul(tile[t], ((t >> j) & 1) ? d1 : d0);
+      }
+    } else if (op.type == D_DIAG2) {
+      const int f0 = op.g0 ? (int)((base >> op.b0) & 1) : -1;
+      const int f1 = op.g1 ? (int)((base >> op.b1) & 1) : -1;
+      for (int t = tid; t < E; t += nt) {
+        const int i0 = f0 >= 0 ? f0 : ((t >> op.b0) & 1);
+        const int i1 = f1 >= 0 ? f1 : ((t >> op.b1) & 1);
+        tile[t] = cmul(tile[t], u[2 * i0 + i1]);
+      }
+    } else {  // D_MAT2, both bits in the tile
+      const int ja = op.b0, jb = op.b1;
+      const int jl = ja < jb ? ja : jb, jh = ja < jb ? jb : ja;
+      for (int p = tid; p < (E >> 2); p += nt) {
+        int t = ((p >> jl) << (jl + 1)) | (p & ((1 << jl) - 1));
+        t = ((t >> jh) << (jh + 1)) | (t & ((1 << jh) - 1));
+        V e[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) e[s] = tile[t | ((s >> 1) << ja) | ((s & 1) << jb)];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          V acc;
+          acc.x = R(0);
+          acc.y = R(0);
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const V w = u[4 * r + s];
+            acc.x += w.x * e[s].x - w.y * e[s].y;
+            acc.y += w.x * e[s].y + w.y * e[s].x;
+          }
+          tile[t | ((r >> 1) << ja) | ((r & 1) << jb)] = acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  V* d = dst + state * a.state_elems + base;
+  for (int t = tid; t < E; t += nt) d[(t & cmask) | hi_off[t >> a.c]] = tile[t];
+}
+
+// ---------------------------------------------------------------------------
+// gather: partial[y][i] = sum_{leaf j in group y} w_j * A_j[ia_i] * B_j[ib_i]  (fp64)
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+gather_kernel(const void* A, const void* B, long long a_elems, long long b_elems, int n_leaves,
+              int leaves_per_group, const double* weights, const int32_t* ia, const int32_t* ib,
+              long long n_req, double2* partial) {
+  using V = typename Cx<R>::T;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req) return;
+  const int j0 = blockIdx.y * leaves_per_group;
+  const int j1 = min(n_leaves, j0 + leaves_per_group);
+  const V* pa = reinterpret_cast<const V*>(A) + ia[i];
+  const V* pb = reinterpret_cast<const V*>(B) + ib[i];
+  double re = 0.0, im = 0.0;
+  for (int j = j0; j < j1; ++j) {
+    const V x = pa[(long long)j * a_elems];
+    const V y = pb[(long long)j * b_elems];
+    const double xr = x.x, xi = x.y, yr = y.x, yi = y.y;
+    const double w = weights[j];
+    re += w * (xr * yr - xi * yi);
+    im += w * (xr * yi + xi * yr);
+  }
+  partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
+}
+
+__global__ void __launch_bounds__(256)
+reduce_kernel(const double2* partial, int groups, long long n_req, double2* acc) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req) return;
+  double2 s = acc[i];
+  for (int g = 0; g < groups; ++g) {
+    const double2 p = partial[(long long)g * n_req + i];
+    s.x += p.x;
+    s.y += p.y;
+  }
+  acc[i] = s;
+}
+
+}  // namespace gs

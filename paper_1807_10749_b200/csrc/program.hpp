@@ -1,0 +1,142 @@
+// Host-side program analysis: path-tree levels, segment op lists and the
+// shared-memory pass scheduler.  Pure C++ (no CUDA), so the planning logic is
+// exercised by host-only contexts in the CPU test suite.
+//
+// Reference semantics mirrored here:
+//  * op stream order and tags: `_lower_uncached` (pathsum.py:157-189);
+//  * cross digit k selects term k of the cross gate's Schmidt decomposition,
+//    big-endian mixed radix over gate order (pathsum.py:219-236);
+//  * block-local qubit j lives at bit (q-1-j) of the block index
+//    (`_b_view1`, pathsum.py:450-451).
+// The reference walks the stream op by op, one numpy pass each; here the
+// stream is cut at cross-gate cycles into path-tree levels, and each level's
+// ops are packed into as few full-state passes as locality allows.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace gs {
+
+struct GsError : std::runtime_error {
+  int code;
+  GsError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+enum HostKind { K_DIAG1 = 0, K_MAT1 = 1, K_DIAG2 = 2, K_MAT2 = 3, K_CROSS = 4 };
+
+// One block-local op on state bits (s0, s1); cross ops carry their gate index.
+struct HostOp {
+  int kind;       // K_DIAG1/K_MAT1/K_DIAG2/K_MAT2 (cross ops resolved per side)
+  int s0 = -1, s1 = -1;
+  int64_t coef = 0;  // coefficient pool offset (non-cross)
+  int cross = -1;    // cross gate index (digit-dependent coefficients)
+  bool diag() const { return kind == K_DIAG1 || kind == K_DIAG2; }
+};
+
+struct PassPlan {
+  int k = 0;                    // tile bits
+  std::vector<int> lbits;       // tile bit -> state bit (ascending)
+  std::vector<int> gbits;       // tile-id bit -> state bit (ascending)
+  std::vector<HostOp> ops;      // ops applied in this pass, in order
+  int64_t dev_op_offset = 0;    // into the device op array
+};
+
+struct Level {
+  int k_lo = 0, k_hi = 0;  // cross digits [k_lo, k_hi) introduced at this level
+  std::vector<HostOp> ops[2];
+  std::vector<PassPlan> passes[2];
+};
+
+inline bool ops_conflict(const HostOp& a, const HostOp& b) {
+  if (a.diag() && b.diag()) return false;
+  const int sa[2] = {a.s0, a.s1}, sb[2] = {b.s0, b.s1};
+  for (int x : sa)
+    for (int y : sb)
+      if (x >= 0 && x == y) return true;
+  return false;
+}
+
+// Greedy pass scheduler.  Every pass keeps the low `c` state bits in the tile
+// (coalesced runs of 2^c amplitudes) and fills the rest of the k-bit tile with
+// the qubits of the earliest ready non-diagonal ops.  Diagonal ops need no
+// locality: on a non-tile bit they are a per-tile constant.  An op is deferred
+// when it would overflow the tile or when an earlier deferred op on one of its
+// qubits does not commute with it.
+inline std::vector<PassPlan> schedule_passes(const std::vector<HostOp>& ops, int q, int kmax,
+                                             int cmin, bool force_one) {
+  std::vector<PassPlan> out;
+  const int k = std::min(q, kmax);
+  const int c = std::min(cmin, std::max(0, k - 2));  // leave room for a 2-qubit op
+  std::vector<HostOp> remaining = ops;
+  if (remaining.empty() && force_one) {
+    PassPlan p;
+    p.k = k;
+    for (int s = 0; s < k; ++s) p.lbits.push_back(s);
+    for (int s = k; s < q; ++s) p.gbits.push_back(s);
+    out.push_back(p);
+    return out;
+  }
+  while (!remaining.empty()) {
+    std::vector<char> in_tile(q, 0);
+    int n_tile = 0;
+    for (int s = 0; s < c; ++s) in_tile[s] = 1, ++n_tile;
+    if (k == q) {
+      for (int s = 0; s < q; ++s) in_tile[s] = 1;
+      n_tile = q;
+    }
+    std::vector<char> blk_nd(q, 0), blk_d(q, 0);
+    std::vector<HostOp> taken, deferred;
+    for (const HostOp& op : remaining) {
+      const int bits[2] = {op.s0, op.s1};
+      bool nd_block = false, d_block = false;
+      for (int b : bits)
+        if (b >= 0) nd_block |= blk_nd[b], d_block |= blk_d[b];
+      if (op.diag()) {
+        if (nd_block) {
+          deferred.push_back(op);
+          for (int b : bits)
+            if (b >= 0) blk_d[b] = 1;
+        } else {
+          taken.push_back(op);
+        }
+        continue;
+      }
+      bool ok = !(nd_block || d_block);
+      if (ok) {
+        int need = 0;
+        for (int b : bits)
+          if (b >= 0 && !in_tile[b]) ++need;
+        if (op.s0 >= 0 && op.s1 >= 0 && op.s0 == op.s1) need = in_tile[op.s0] ? 0 : 1;
+        ok = n_tile + need <= k;
+      }
+      if (ok) {
+        for (int b : bits)
+          if (b >= 0 && !in_tile[b]) in_tile[b] = 1, ++n_tile;
+        taken.push_back(op);
+      } else {
+        deferred.push_back(op);
+        for (int b : bits)
+          if (b >= 0) blk_nd[b] = 1;
+      }
+    }
+    if (taken.empty()) throw GsError(-1, "pass scheduler made no progress");
+    // fill unused tile slots with the lowest remaining bits (wider contiguous runs)
+    for (int s = 0; s < q && n_tile < k; ++s)
+      if (!in_tile[s]) in_tile[s] = 1, ++n_tile;
+    PassPlan p;
+    p.k = k;
+    for (int s = 0; s < q; ++s) (in_tile[s] ? p.lbits : p.gbits).push_back(s);
+    p.ops = std::move(taken);
+    out.push_back(std::move(p));
+    remaining = std::move(deferred);
+  }
+  return out;
+}
+
+}  // namespace gs

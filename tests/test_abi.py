@@ -1,0 +1,118 @@
+"""The C ABI library: loads, exports every declared symbol, and its host-side
+planning (path-tree enumeration, pass scheduling, error mapping) is exercised
+through host-only contexts (device = -1: no kernels, no GPU needed)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1807_10749_b200 import CircuitError, configs, make_plan, split_requests
+from paper_1807_10749_b200.lowering import lowered
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_1807_10749_b200 import engine
+
+    with open(os.path.join(ROOT, "include", "gridsim_b200.h")) as fh:
+        header = fh.read()
+    declared = set(re.findall(r"\b(gs_[a-z_]+)\s*\(", header))
+    assert declared == set(engine.EXPORTED_SYMBOLS)
+    for name in declared:
+        assert hasattr(engine.LIB, name), name
+    assert engine.LIB.gs_abi_version() == 1
+
+
+def host_engine(dtype="c64"):
+    from paper_1807_10749_b200.engine import Engine
+
+    return Engine(device=-1, dtype=dtype)
+
+
+def expected_nodes(circ, plan, prefixes, branch_lo=0, branch_hi=None):
+    """Distinct digit prefixes per level (the path tree), counted in Python."""
+    radices = plan.radices
+    prog = lowered(circ, plan.cut)
+    cyc = prog.cross_cycle
+    ends = [k + 1 for k in range(len(cyc)) if k + 1 == len(cyc) or cyc[k + 1] != cyc[k]]
+    bs = plan.branch_space
+    branch_hi = bs if branch_hi is None else branch_hi
+    paths = [int(p) * bs + b for p in sorted(prefixes) for b in range(branch_lo, branch_hi)]
+    total = 1  # root
+    for li, e in enumerate(ends):
+        suffix = int(np.prod(radices[e:], dtype=object)) if e < len(radices) else 1
+        keys = [p // suffix for p in paths]
+        total += len(keys) if li == len(ends) - 1 else len(set(keys))
+    return total, len(paths), len(ends) + 1
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg1v2", "cfg2", "cfg3"])
+def test_dry_run_tree_counts(name):
+    circ, plan, req, pre = configs.build(name, n_req=16)
+    if name == "cfg3":
+        pre = pre[:300]
+    eng = host_engine()
+    eng.load_program(lowered(circ, plan.cut))
+    ia, ib = split_requests(circ.n_qubits, plan.cut.block_a, plan.cut.block_b, req)
+    eng.set_requests(ia, ib)
+    st = eng.run(plan.x_p, pre, 0, plan.branch_space).stats
+    nodes, leaves, levels = expected_nodes(circ, plan, pre)
+    assert st["n_paths"] == leaves
+    assert st["n_nodes"] == nodes
+    assert st["n_levels"] == levels
+    # a branch sub-range and another split enumerate the same leaves
+    st2 = eng.run(plan.x_p, pre[:3], 1, plan.branch_space).stats
+    assert st2["n_paths"] == 3 * (plan.branch_space - 1)
+    p0 = make_plan(circ, x_p=0, cut=plan.cut) if plan.x <= 20 else None
+    if p0 is not None:
+        st3 = eng.run(0, [0], 0, p0.branch_space).stats
+        assert st3["n_paths"] == p0.branch_space
+
+
+def test_dry_run_duplicates_and_unsorted():
+    circ, plan, req, _ = configs.build("cfg1v2", n_req=4)
+    eng = host_engine()
+    eng.load_program(lowered(circ, plan.cut))
+    eng.set_requests(*split_requests(16, plan.cut.block_a, plan.cut.block_b, req))
+    pre = np.array([5, 3, 5, 9], dtype=np.int64)
+    st = eng.run(plan.x_p, pre, 0, plan.branch_space).stats
+    assert st["n_paths"] == 4 * plan.branch_space
+    flat = make_plan(circ, x_b=0)
+    st = eng.run(flat.x_p, np.array([7, 7, 2]), 0, 1).stats
+    assert st["n_paths"] == 3
+
+
+def test_error_mapping():
+    circ, plan, req, _ = configs.build("cfg1", n_req=4)
+    eng = host_engine()
+    with pytest.raises(RuntimeError):
+        eng.run(plan.x_p, plan.retained, 0, plan.branch_space)  # no program
+    eng.load_program(lowered(circ, plan.cut))
+    with pytest.raises(IndexError):
+        eng.set_requests(np.array([256]), np.array([0]))
+    eng.set_requests(np.array([0, 1]), np.array([2, 3]))
+    with pytest.raises(CircuitError):
+        eng.run(plan.x + 1, [0], 0, 1)
+    with pytest.raises(ValueError):
+        eng.run(plan.x_p, [plan.prefix_space], 0, plan.branch_space)
+    with pytest.raises(ValueError):
+        eng.run(plan.x_p, [0], 0, plan.branch_space + 1)
+    with pytest.raises(ValueError):
+        eng.set_option("no_such_option", 1)
+    with pytest.raises(ValueError):
+        eng.set_option("tile_bits", 40)
+
+
+@pytest.mark.parametrize("tile_bits", [4, 5, 8, 13])
+def test_scheduler_covers_all_ops(tile_bits):
+    """Smaller tiles split levels into more passes; every op is still scheduled once."""
+    circ, plan, req, pre = configs.build("cfg2", n_req=4)
+    eng = host_engine()
+    eng.set_option("tile_bits", tile_bits)
+    eng.load_program(lowered(circ, plan.cut))
+    eng.set_requests(np.array([0]), np.array([0]))
+    st = eng.run(plan.x_p, pre[:64], 0, plan.branch_space).stats
+    assert st["n_paths"] == 64 * plan.branch_space
+    assert st["n_pass_launches"] >= 2 * st["n_levels"]

@@ -1,0 +1,135 @@
+"""GPU parity: the CUDA path through the C ABI vs the reference's own outputs.
+
+Bars (BASELINE.json north_star): complex64 within 1e-5 relative L2 of the
+reference run_approx / run_batched / run_path; complex128 within 1e-10 of the
+reference with DTYPE rebound to complex128; path enumeration and subset are
+bit-exact (the plan is the reference's, tests/test_plan.py).
+"""
+import numpy as np
+import pytest
+
+from conftest import load_amps, rel_l2, small_case
+from paper_1807_10749_b200 import configs, make_plan
+
+pytestmark = pytest.mark.gpu
+
+C64_TOL = 1e-5
+C128_TOL = 1e-10
+SMALL = ["s3x4v2", "s3x4v1", "s4x4v2", "stair3x4", "iswap2x3", "iswap3x3", "fsim3x4", "fsim2x4"]
+
+
+@pytest.fixture(scope="module")
+def ps():
+    from paper_1807_10749_b200 import engine, pathsum
+
+    if engine.device_count() < 1:
+        pytest.fail("no CUDA device visible to libgridsim_b200.so")
+    return pathsum
+
+
+def _engine(dtype="c64"):
+    from paper_1807_10749_b200.engine import ENGINES
+
+    return ENGINES.get(0, dtype)
+
+
+@pytest.fixture(params=[0, 5, 4])
+def tile_bits(request):
+    """0 = default tile; 5/4 force multi-pass schedules with out-of-tile diagonal ops."""
+    eng64, eng128 = _engine("c64"), _engine("c128")
+    for e in (eng64, eng128):
+        e.set_option("tile_bits", request.param)
+    yield request.param
+    for e in (eng64, eng128):
+        e.set_option("tile_bits", 0)
+
+
+def test_cz2_known_answer(ps):
+    circ, plan, idx, g = small_case("cz2")
+    np.testing.assert_allclose(ps.run_approx(circ, plan, idx).amps, [0.5, 0.5, 0.5, -0.5], atol=1e-7)
+    np.testing.assert_allclose(ps.run_prefix_tree(circ, plan, 0, idx).amps, g["path0"], atol=1e-7)
+    np.testing.assert_allclose(ps.run_prefix_tree(circ, plan, 1, idx).amps, g["path1"], atol=1e-7)
+
+
+@pytest.mark.parametrize("case", SMALL)
+def test_small_cases(ps, case, tile_bits):
+    circ, plan, idx, g = small_case(case)
+    assert rel_l2(ps.run_approx(circ, plan, idx).amps, g["amps_c64"]) <= C64_TOL
+    assert rel_l2(ps.run_approx(circ, plan, idx, dtype="c128").amps, g["amps_c128"]) <= C128_TOL
+    for pid, want in zip(g["path_ids"], g["path_amps"]):
+        assert rel_l2(ps.run_path(circ, plan, int(pid), idx).amps, want) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg1v2"])
+def test_cfg1(ps, name, tile_bits):
+    g = load_amps(name)
+    circ, plan, req, _ = configs.build(name)
+    assert rel_l2(ps.run_approx(circ, plan, req).amps, g["amps_c64"]) <= C64_TOL
+    assert rel_l2(ps.run_approx(circ, plan, req, dtype="c128").amps, g["amps_c128"]) <= C128_TOL
+    assert rel_l2(ps.run_approx(circ, plan, req).amps, g["full_c64"]) <= C64_TOL
+    for pid, want in zip(g["path_ids"], g["path_amps"]):
+        assert rel_l2(ps.run_path(circ, plan, int(pid), req).amps, want) <= C64_TOL
+    pq = make_plan(circ, fidelity=0.25, seed=5)
+    assert rel_l2(ps.run_approx(circ, pq, req).amps, g["f025_amps"]) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg2v2", "cfg2h", "cfg3", "cfg3v2", "cfg4"])
+def test_config_windows(ps, name):
+    g = load_amps(name)
+    circ, plan, _, _ = configs.build(name, n_req=4)
+    req = g["requests"]
+    got = ps.run_batched(circ, plan, req, prefixes=g["prefixes"]).amps
+    assert rel_l2(got, g["amps_c64"]) <= C64_TOL
+    if "amps_c128" in g:
+        got = ps.run_batched(circ, plan, req, prefixes=g["prefixes_c128"], dtype="c128").amps
+        assert rel_l2(got, g["amps_c128"]) <= C128_TOL
+    if "path_ids" in g:
+        for pid, want in zip(g["path_ids"], g["path_amps"]):
+            assert rel_l2(ps.run_path(circ, plan, int(pid), req).amps, want) <= C64_TOL
+
+
+def test_split_invariance_and_order(ps):
+    circ, plan, req, _ = configs.build("cfg1v2")
+    base = ps.run_approx(circ, make_plan(circ, x_b=0), req).amps
+    for x_p in (0, 2, 5, 8):
+        got = ps.run_approx(circ, make_plan(circ, x_p=x_p), req).amps
+        assert rel_l2(got, base) <= 1e-6
+    fwd = ps.run_batched(circ, plan, req, prefixes=plan.retained).amps
+    bwd = ps.run_batched(circ, plan, req, prefixes=plan.retained[::-1]).amps
+    assert rel_l2(fwd, bwd) <= 1e-12
+
+
+def test_linearity_and_duplicates(ps):
+    """Sum over a prefix set = sum of the sums over a partition; duplicates count twice."""
+    circ, plan, req, _ = configs.build("cfg2")
+    pre = plan.retained[:512]
+    whole = ps.run_batched(circ, plan, req, prefixes=pre).amps
+    parts = sum(ps.run_batched(circ, plan, req, prefixes=p).amps for p in np.array_split(pre, 3))
+    assert rel_l2(parts, whole) <= 1e-10
+    dup = ps.run_batched(circ, plan, req, prefixes=np.concatenate([pre[:7], pre[:7]])).amps
+    one = ps.run_batched(circ, plan, req, prefixes=pre[:7]).amps
+    assert rel_l2(dup, 2 * one) <= 1e-12
+
+
+def test_cfg2_full_job_is_exact_state(ps):
+    """f = 1: all 262,144 paths of config 2 sum to the exact amplitudes."""
+    g = load_amps("cfg2_full")
+    circ, plan, req, _ = configs.build("cfg2")
+    got = ps.run_approx(circ, plan, req).amps
+    assert rel_l2(got, g["exact"]) <= C64_TOL
+
+
+def test_errors(ps):
+    circ, plan, req, _ = configs.build("cfg1")
+    with pytest.raises(ValueError):
+        ps.run_approx(circ, plan, req, engine="nope")
+    with pytest.raises(IndexError):
+        ps.run_approx(circ, plan, [1 << 16])
+    with pytest.raises(ValueError):
+        ps.run_batched(circ, plan, req, prefixes=[plan.prefix_space])
+    with pytest.raises(ValueError):
+        ps.run_path(circ, plan, plan.path_space, req)
+    empty = ps.run_approx(circ, plan, np.array([], dtype=np.int64))
+    assert empty.amps.shape == (0,)
+    none = ps.run_batched(circ, plan, req, prefixes=np.array([], dtype=np.int64))
+    assert np.all(none.amps == 0)

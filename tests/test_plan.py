@@ -1,0 +1,182 @@
+"""Host planning vs the reference: bit-exact enumeration and subset selection.
+
+Pins plan.py / circuit.py / requests.py against plans the reference itself
+produced (tests/golden/plans.json) and against the reference's own unit tests
+(test_pathsum.py:37-157).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from paper_1807_10749_b200 import (
+    CircuitError,
+    Gate,
+    GateKind,
+    all_cuts,
+    challenge_indices,
+    circuit_hash,
+    gate_matrix,
+    make_plan,
+    parse_circuit,
+    path_digits,
+    path_id,
+    retained_prefixes,
+    schmidt_decompose,
+    serialize_circuit,
+    split_requests,
+)
+from paper_1807_10749_b200 import configs
+
+
+def sha(arr):
+    return hashlib.sha256(np.ascontiguousarray(arr, dtype=np.int64).tobytes()).hexdigest()
+
+
+CHEAP = ["cfg1", "cfg1v2", "cfg2", "cfg2v2", "cfg2h", "cfg3", "cfg3v2", "cfg4", "cfg4v2"]
+
+
+@pytest.mark.parametrize("name", CHEAP + ["cfg5f"])
+def test_circuit_fixture_hash(name, plans_golden):
+    spec = configs.CONFIGS[name]
+    circ = configs.load_circuit(spec)
+    assert circuit_hash(circ) == plans_golden[name]["circuit_hash"]
+    assert parse_circuit(serialize_circuit(circ), spec.rows, spec.cols) == circ
+
+
+@pytest.mark.parametrize("name", CHEAP)
+def test_plan_matches_reference(name, plans_golden):
+    gold = plans_golden[name]
+    spec = configs.CONFIGS[name]
+    circ = configs.load_circuit(spec)
+    plan = make_plan(circ, fidelity=spec.fidelity, seed=0, cut=configs.config_cut(spec, circ))
+    assert list(plan.cut.block_a) == gold["cut"][2]
+    assert list(plan.cut.block_b) == gold["cut"][3]
+    if spec.cut == "default":
+        assert [plan.cut.orientation, plan.cut.position] == gold["cut"][:2]
+    assert list(plan.radices) == gold["radices"]
+    assert (plan.x_p, plan.x_b, plan.d_p, plan.d_b) == (gold["x_p"], gold["x_b"], gold["d_p"], gold["d_b"])
+    assert plan.retained.size == gold["n_retained"]
+    assert sha(plan.retained) == gold["retained_sha256"]
+    if "retained" in gold:
+        np.testing.assert_array_equal(plan.retained, gold["retained"])
+    if "workers8" in gold:
+        p8 = make_plan(circ, fidelity=spec.fidelity, seed=0, cut=configs.config_cut(spec, circ), workers=8)
+        assert (p8.x_p, p8.x_b) == (gold["workers8"]["x_p"], gold["workers8"]["x_b"])
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg5v2"])
+def test_cfg5_retained_head_matches_reference(name, plans_golden):
+    gold = plans_golden[name]
+    circ, plan, _, pre = configs.build(name, n_req=4)
+    assert list(plan.radices) == gold["radices"]
+    assert (plan.x_p, plan.x_b) == (gold["x_p"], gold["x_b"])
+    np.testing.assert_array_equal(plan.retained[:64], gold["retained_head"])
+    assert pre.size * plan.branch_space == 1 << 16
+
+
+def test_cfg5f_plan(plans_golden):
+    gold = plans_golden["cfg5f"]
+    circ, plan, _, pre = configs.build("cfg5f", n_req=4)
+    assert list(plan.radices) == gold["radices"] and set(plan.radices) == {4}
+    np.testing.assert_array_equal(plan.retained, gold["retained"])
+    assert pre.size * plan.branch_space == 1 << 16
+
+
+@pytest.mark.parametrize("name", CHEAP)
+def test_requests_and_split(name, plans_golden):
+    gold = plans_golden[name]
+    spec = configs.CONFIGS[name]
+    circ = configs.load_circuit(spec)
+    req = challenge_indices(circ.n_qubits, spec.n_req, 12345)
+    assert sha(req) == gold["requests_sha256"]
+    cut_a, cut_b = gold["cut"][2], gold["cut"][3]
+    ia, ib = split_requests(circ.n_qubits, tuple(cut_a), tuple(cut_b), req[:256])
+    np.testing.assert_array_equal(ia, gold["split_head"][0])
+    np.testing.assert_array_equal(ib, gold["split_head"][1])
+
+
+# --- reference unit tests restated (test_pathsum.py:37-157) ---------------------------
+
+def _recon(terms):
+    return sum(np.kron(l, r) for l, r in terms)
+
+
+def test_cz_is_projector_pair():
+    dec = schmidt_decompose(GateKind.CZ)
+    assert dec.rank == 2
+    np.testing.assert_allclose(dec.terms[0][0], np.diag([1.0, 0.0]))
+    np.testing.assert_allclose(dec.terms[1][1], np.diag([1.0, -1.0]))
+
+
+def test_iswap_and_random_reconstruct():
+    g = Gate(0, GateKind.ISWAP, (0, 1))
+    assert schmidt_decompose(g).rank == 4
+    np.testing.assert_allclose(_recon(schmidt_decompose(g).terms), gate_matrix(g), atol=1e-12)
+    rng = np.random.default_rng(8)
+    u, _ = np.linalg.qr(rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4)))
+    dec = schmidt_decompose(u)
+    np.testing.assert_allclose(_recon(dec.terms), u, atol=1e-10)
+    assert schmidt_decompose(np.eye(4)).rank == 1
+    assert schmidt_decompose(np.eye(4)[[0, 2, 1, 3]]).rank == 4
+    with pytest.raises(ValueError):
+        schmidt_decompose(np.eye(2))
+
+
+def test_retained_count_and_rounding():
+    for space in (8, 32, 1024, 4096):
+        for f in (1.0, 0.5, 0.25, 0.125, 0.01, 1e-6):
+            assert len(retained_prefixes(space, f, seed=7)) == max(1, round(f * space))
+    assert len(retained_prefixes(1024, 0.0051, seed=0)) == 5
+    got = retained_prefixes(4096, 0.3, seed=11)
+    assert np.all(np.diff(got) > 0)
+    np.testing.assert_array_equal(retained_prefixes(64, 1.0, 0), np.arange(64))
+    with pytest.raises(CircuitError):
+        retained_prefixes(4, 1.3, 0)
+
+
+def test_plan_errors():
+    circ = configs.load_circuit(configs.CONFIGS["cfg1v2"])
+    with pytest.raises(CircuitError):
+        make_plan(circ, x_p=1, x_b=1)
+    with pytest.raises(CircuitError):
+        make_plan(circ, fidelity=0.0)
+    with pytest.raises(CircuitError):
+        make_plan(circ, fidelity=1.5)
+    cut = all_cuts(circ)[0]
+    assert make_plan(circ, cut=cut, x_b=0).cut == cut
+
+
+def test_path_digits_round_trip():
+    radices = (2, 4, 2, 4)
+    for pid in range(64):
+        assert path_id(path_digits(pid, radices), radices) == pid
+    with pytest.raises(ValueError):
+        path_digits(64, radices)
+    with pytest.raises(ValueError):
+        path_id((2, 0, 0, 0), radices)
+
+
+def test_split_bit_layouts():
+    idx = np.arange(16, dtype=np.int64)
+    a, b = split_requests(4, (0, 1), (2, 3), idx)
+    np.testing.assert_array_equal(a, idx >> 2)
+    np.testing.assert_array_equal(b, idx & 3)
+    a, b = split_requests(4, (0, 2), (1, 3), idx)
+    np.testing.assert_array_equal(a, ((idx >> 3) & 1) << 1 | ((idx >> 1) & 1))
+    np.testing.assert_array_equal(b, ((idx >> 2) & 1) << 1 | (idx & 1))
+    with pytest.raises(IndexError):
+        split_requests(4, (0, 1), (2, 3), [16])
+    with pytest.raises(IndexError):
+        split_requests(4, (0, 1), (2, 3), [-1])
+
+
+def test_parse_errors():
+    from paper_1807_10749_b200 import ParseError
+
+    for text in ("", "x\n", "2\n0 h\n", "2\n0 foo 1\n", "2\n0 h 0 1\n", "2\n0 cz 0 0\n",
+                 "2\n0 h 5\n", "2\nq h 0\n"):
+        with pytest.raises(CircuitError):
+            parse_circuit(text)
+    with pytest.raises(ParseError):
+        parse_circuit("2\n0 g2 0 1 1 0\n")
