@@ -34,6 +34,14 @@ namespace gs {
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
   ~DevBuf() { release(); }
   void release() {
     if (p) cudaFree(p);
@@ -57,6 +65,10 @@ struct DevBuf {
 struct PinnedBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  PinnedBuf(PinnedBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
   ~PinnedBuf() {
     if (p) cudaFreeHost(p);
   }
@@ -390,6 +402,14 @@ static void enumerate_children(Ctx& c, int l, const Node* parents, int64_t n_par
 // ---------------------------------------------------------------------------
 // launches
 
+static void launch_check(const char* what, int64_t blocks, int threads, size_t smem) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    throw GsError(GS_ERR_CUDA, std::string(what) + " launch (" + std::to_string(blocks) + " blocks x " +
+                                   std::to_string(threads) + " threads, " + std::to_string(smem) +
+                                   " B smem): " + cudaGetErrorString(e));
+}
+
 template <typename R>
 static void launch_pass(Ctx& c, int side, const PassPlan& pp, const void* src, void* dst,
                         const int32_t* parent, const int32_t* digit, int64_t n_states,
@@ -425,7 +445,7 @@ static void launch_pass(Ctx& c, int side, const PassPlan& pp, const void* src, v
   c.st.pass_amp_updates += (double)n_states * (double)(1LL << q);
   if (c.host_only) return;
   gate_pass_kernel<R><<<(unsigned)blocks, threads, smem, c.stream>>>(a);
-  CK(cudaGetLastError());
+  launch_check("gate_pass_kernel", blocks, threads, smem);
 }
 
 struct Timer {
@@ -507,11 +527,11 @@ template <typename R> static void gather(Ctx& c, int l, const std::vector<Node>&
       c.lvl_a[l].p, c.lvl_b[l].p, 1LL << qa, 1LL << qb, (int)n, (int)per,
       reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const int32_t*>(c.d_ia.p),
       reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
-  CK(cudaGetLastError());
+  launch_check("gather_kernel", xblocks * groups, threads, 0);
   reduce_kernel<<<(unsigned)xblocks, threads, 0, c.stream>>>(
       reinterpret_cast<const double2*>(c.d_partial.p), (int)groups, nreq,
       reinterpret_cast<double2*>(c.d_acc.p));
-  CK(cudaGetLastError());
+  launch_check("reduce_kernel", xblocks, threads, 0);
   c.st.n_gather_launches += 2;
   c.st.n_launches += 2;
   c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
