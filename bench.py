@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0)
+    ap.add_argument("--opt", action="append", default=[], help="engine option key=value")
     return ap.parse_args()
 
 
@@ -202,6 +203,9 @@ def main():
     all_windows = [rank_windows(r) for r in range(world)] if world > 1 else [windows]
 
     eng = ENGINES.get(local, args.dtype)
+    for kv in args.opt:
+        key, val = kv.split("=")
+        eng.set_option(key, int(val))
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     prog = lowered(circ, plan.cut)

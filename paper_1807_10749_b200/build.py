@@ -17,8 +17,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libgridsim_b200.so")
-SOURCES = ["engine.cu"]
-DEPS = ["engine.cu", "kernels.cuh", "program.hpp"]
+SOURCES = ["engine.cu", "pass_kernels.cu"]
+DEPS = ["engine.cu", "pass_kernels.cu", "kernels.cuh", "program.hpp", "pass_kernel.cuh",
+        "pass_kernel.h", "pass_types.h"]
 
 NVCC_FLAGS = [
     "-O3",
@@ -27,10 +28,9 @@ NVCC_FLAGS = [
     "-lineinfo",
     "-Xcompiler", "-fPIC",
     "-Xcompiler", "-O2",
-    "-shared",
-    "-cudart", "static",
     "-Xptxas", "-v",
 ]
+LINK_FLAGS = ["-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def nvcc_path() -> str:
@@ -51,13 +51,29 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-o", OUT + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    nvcc = nvcc_path()
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, src)]
+        procs.append((src, obj, subprocess.Popen(cmd, cwd=CSRC, stdout=subprocess.PIPE,
+                                                 stderr=subprocess.PIPE, text=True)))
+    objs = []
+    for src, obj, p in procs:
+        out, err = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError(f"nvcc failed on {src}")
+        if verbose:
+            sys.stderr.write(err)
+        objs.append(obj)
+    cmd = [nvcc, *LINK_FLAGS, "-o", OUT + ".tmp", *objs]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed for libgridsim_b200.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc link failed for libgridsim_b200.so")
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

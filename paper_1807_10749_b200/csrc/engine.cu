@@ -20,6 +20,7 @@
 
 #include "../../include/gridsim_b200.h"
 #include "kernels.cuh"
+#include "pass_kernel.h"
 #include "program.hpp"
 
 namespace gs {
@@ -124,8 +125,13 @@ struct Ctx {
   // program
   bool have_prog = false;
   Program prog;
-  DevBuf d_ops, d_coef, d_xtable;
+  DevBuf d_ops, d_coef, d_xtable, d_pops, d_pstages;
   std::vector<DevOp> host_devops;
+  std::vector<POp> host_pops;
+  std::vector<PStage> host_pstages;
+  double kfinal[2][2] = {{1, 0}, {1, 0}};  // per block: true = stored * K
+  int kernel_version = 2;
+  int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
   // requests
   int64_t n_req = -1;
   DevBuf d_ia, d_ib, d_acc, d_partial;
@@ -164,6 +170,23 @@ static int64_t coef_entries(int kind) {
     case K_MAT2: return 16;
   }
   return 0;
+}
+
+// u = s * W with W one of H=[[1,1],[1,-1]], X=[[1,-i],[-i,1]], Y=[[1,-1],[1,1]]
+// (the reference's H, X^1/2, Y^1/2, circuit.py:46-50); s = u00 is deferred.
+static void classify_w(HostOp& op, const double* u) {
+  const double sr = u[0], si = u[1];
+  const double mag = std::sqrt(sr * sr + si * si);
+  if (mag == 0) return;
+  const double tol = 1e-12 * mag;
+  auto eq = [&](int e, double re, double im) {
+    return std::fabs(u[2 * e] - re) <= tol && std::fabs(u[2 * e + 1] - im) <= tol;
+  };
+  // candidates: (u01, u10, u11) as multiples of s
+  if (eq(1, sr, si) && eq(2, sr, si) && eq(3, -sr, -si)) op.w = 0;                 // H
+  else if (eq(1, si, -sr) && eq(2, si, -sr) && eq(3, sr, si)) op.w = 1;           // X: -i*s
+  else if (eq(1, -sr, -si) && eq(2, sr, si) && eq(3, sr, si)) op.w = 2;           // Y
+  if (op.w >= 0) op.s_re = sr, op.s_im = si;
 }
 
 static void build_program(Ctx& c, int qa, int qb, int n_ops, const int32_t* kind,
@@ -271,6 +294,7 @@ static void build_program(Ctx& c, int qa, int qb, int n_ops, const int32_t* kind
     }
     op.coef = coef_off[i];
     check_coef(op.coef, coef_entries(kd));
+    if (kd == K_MAT1) classify_w(op, coef + 2 * op.coef);
     // level = number of cross cycles <= this op's cycle
     const int l = (int)(std::upper_bound(lvl_cycle.begin(), lvl_cycle.end(), cycle[i]) - lvl_cycle.begin());
     p.levels[l].ops[side].push_back(op);
@@ -322,6 +346,82 @@ static void schedule_program(Ctx& c) {
       }
     }
   }
+  // v2: register stages per pass, W scalars folded into one constant per block
+  c.host_pops.clear();
+  c.host_pstages.clear();
+  for (int side = 0; side < 2; ++side) {
+    double kre = 1.0, kim = 0.0;  // true amplitude = stored * K
+    for (size_t l = 0; l < p.levels.size(); ++l) {
+      Level& L = p.levels[l];
+      for (PassPlan& pp : L.passes[side]) {
+        // register bits per stage: 5 (c64) / 4 (c128); tiny states (< 4 qubits in
+        // the tile) keep the v1 shared-memory kernel
+        pp.M = (c.precision == GS_C64 && pp.k >= 5 && c.reg_bits != 4) ? 5 : (pp.k >= 4 ? 4 : 0);
+        if (pp.M == 0) continue;
+        pp.stages = schedule_stages(pp, pp.M);
+        pp.dev_stage_offset = (int64_t)c.host_pstages.size();
+        std::vector<int> tpos(p.q[side], -1);
+        for (int j = 0; j < (int)pp.lbits.size(); ++j) tpos[pp.lbits[j]] = j;
+        for (const StagePlan& sp : pp.stages) {
+          PStage ps{};
+          std::vector<int> rpos(pp.k, -1);
+          for (int i = 0; i < (int)sp.rb.size(); ++i) ps.rb[i] = (int8_t)sp.rb[i], rpos[sp.rb[i]] = i;
+          ps.op_begin = (int32_t)c.host_pops.size();
+          for (const HostOp& op : sp.ops) {
+            POp d{};
+            d.xtab = -1;
+            d.xstride = 1;
+            d.xradix = 1;
+            d.coef = (int32_t)op.coef;
+            d.w = (int8_t)op.w;
+            if (op.cross >= 0) {
+              d.xtab = p.xtab[side][op.cross];
+              int64_t stride = 1;
+              for (int k = op.cross + 1; k < L.k_hi; ++k) stride *= p.radix[k];
+              d.xstride = (int32_t)stride;
+              d.xradix = p.radix[op.cross];
+            }
+            auto enc = [&](int sb, int8_t& where, int8_t& idx) {
+              if (sb < 0) { where = B_REG; idx = 0; return; }
+              const int t = tpos[sb];
+              if (t >= 0 && rpos[t] >= 0) { where = B_REG; idx = (int8_t)rpos[t]; }
+              else if (t >= 0) { where = B_THREAD; idx = (int8_t)t; }
+              else { where = B_TILE; idx = (int8_t)sb; }
+            };
+            enc(op.s0, d.where0, d.idx0);
+            enc(op.s1, d.where1, d.idx1);
+            switch (op.kind) {
+              case K_MAT1: d.type = (op.w >= 0) ? P_W : P_M1; break;
+              case K_DIAG1: d.type = P_D1; break;
+              case K_DIAG2: d.type = P_D2; break;
+              default: d.type = P_M2; break;
+            }
+            if ((d.type == P_W || d.type == P_M1 || d.type == P_M2) &&
+                (d.where0 != B_REG || (d.type == P_M2 && d.where1 != B_REG)))
+              throw GsError(GS_ERR_ARG, "stage scheduler placed a dense op outside the registers");
+            if (op.w >= 0) {  // K *= s
+              const double r = kre * op.s_re - kim * op.s_im, i = kre * op.s_im + kim * op.s_re;
+              kre = r, kim = i;
+            }
+            c.host_pops.push_back(d);
+          }
+          ps.op_end = (int32_t)c.host_pops.size();
+          c.host_pstages.push_back(ps);
+        }
+        // power-of-two rescale on store keeps |stored| ~ |true amplitude|
+        const double mag = std::sqrt(kre * kre + kim * kim);
+        const int e = (int)std::lround(std::log2(mag));
+        pp.store_scale = 1.0;
+        if (std::abs(e) >= 16) {
+          pp.store_scale = std::ldexp(1.0, e);
+          kre = std::ldexp(kre, -e);
+          kim = std::ldexp(kim, -e);
+        }
+      }
+    }
+    c.kfinal[side][0] = kre;
+    c.kfinal[side][1] = kim;
+  }
   // level digit products must fit int32 node digits
   for (size_t l = 1; l < p.levels.size(); ++l) {
     int64_t f = 1;
@@ -340,6 +440,8 @@ template <typename T> static void upload(Ctx& c, DevBuf& b, const std::vector<T>
 static void upload_program(Ctx& c) {
   if (c.host_only) return;
   upload(c, c.d_ops, c.host_devops);
+  upload(c, c.d_pops, c.host_pops);
+  upload(c, c.d_pstages, c.host_pstages);
   upload(c, c.d_xtable, c.prog.xtable);
   if (c.precision == GS_C64) {
     std::vector<float> f(c.prog.coef.begin(), c.prog.coef.end());
@@ -448,6 +550,69 @@ static void launch_pass(Ctx& c, int side, const PassPlan& pp, const void* src, v
   launch_check("gate_pass_kernel", blocks, threads, smem);
 }
 
+static int ceil_log2(int64_t n) {
+  int b = 0;
+  while ((1LL << b) < n) ++b;
+  return b;
+}
+
+template <typename R, int M>
+static void launch_pass2_m(Ctx& c, const Pass2Args& a, int64_t blocks, int threads, size_t smem) {
+  const cudaError_t e = launch_pass2_kernel(sizeof(R) == 4 ? 0 : 1, M, a, (unsigned)blocks, threads, smem, c.stream);
+  if (e != cudaSuccess) cudaGetLastError();
+  if (e != cudaSuccess)
+    throw GsError(GS_ERR_CUDA, "pass2_kernel launch (" + std::to_string(blocks) + " blocks x " +
+                                   std::to_string(threads) + " threads, " + std::to_string(smem) +
+                                   " B smem): " + cudaGetErrorString(e));
+}
+
+template <typename R>
+static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, void* dst,
+                         const int32_t* parent, const int32_t* digit, int64_t n_states,
+                         bool init_zero) {
+  const int q = c.prog.q[side];
+  Pass2Args a{};
+  a.src = src;
+  a.dst = dst;
+  a.parent = parent;
+  a.digit = digit;
+  a.ops = reinterpret_cast<const POp*>(c.d_pops.p);
+  a.stages = reinterpret_cast<const PStage*>(c.d_pstages.p) + pp.dev_stage_offset;
+  a.coefs = c.d_coef.p;
+  a.xtable = reinterpret_cast<const int32_t*>(c.d_xtable.p);
+  a.state_elems = 1LL << q;
+  a.n_states = n_states;
+  a.store_scale = pp.store_scale;
+  a.n_stages = (int)pp.stages.size();
+  a.kq = pp.k;
+  const int kcap = std::min(c.kmax(), pp.M + 8);
+  const int slots = std::max(0, std::min(kcap - pp.k, ceil_log2(n_states)));
+  a.K = pp.k + slots;
+  int cc = 0;
+  while (cc < pp.k && pp.lbits[cc] == cc) ++cc;
+  a.c = std::min(cc, 10);
+  a.tiles_log = q - pp.k;
+  a.init_zero = init_zero ? 1 : 0;
+  a.n_hi = 1 << (pp.k - a.c);
+  for (int j = 0; j < pp.k; ++j) a.lbits[j] = pp.lbits[j];
+  for (int j = 0; j < (int)pp.gbits.size(); ++j) a.gbits[j] = pp.gbits[j];
+  const int threads = 1 << (a.K - pp.M);
+  const size_t smem = ((size_t)1 << a.K) * c.esize() + (size_t)a.n_hi * sizeof(int);
+  const int64_t groups = (n_states + (1LL << slots) - 1) >> slots;
+  const int64_t blocks = groups << a.tiles_log;
+  if (blocks > INT32_MAX) throw GsError(GS_ERR_ARG, "grid too large");
+  c.st.n_pass_launches++;
+  c.st.n_launches++;
+  c.st.pass_bytes += 2.0 * (double)n_states * (double)(1LL << q) * (double)c.esize();
+  c.st.pass_amp_updates += (double)n_states * (double)(1LL << q);
+  if (c.host_only) return;
+  if (pp.M == 5) {
+    if constexpr (sizeof(R) == 4) launch_pass2_m<R, 5>(c, a, blocks, threads, smem);
+  } else {
+    launch_pass2_m<R, 4>(c, a, blocks, threads, smem);
+  }
+}
+
 struct Timer {
   Ctx& c;
   double* acc;
@@ -483,8 +648,12 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
   for (int side = 0; side < 2; ++side) {
     bool first = true;
     for (const PassPlan& pp : L.passes[side]) {
-      launch_pass<R>(c, side, pp, first ? srcs[side] : dsts[side], dsts[side],
-                     first ? parent : nullptr, digit, n, root && first);
+      if (c.kernel_version == 2 && pp.M > 0)
+        launch_pass2<R>(c, side, pp, first ? srcs[side] : dsts[side], dsts[side],
+                        first ? parent : nullptr, digit, n, root && first);
+      else
+        launch_pass<R>(c, side, pp, first ? srcs[side] : dsts[side], dsts[side],
+                       first ? parent : nullptr, digit, n, root && first);
       first = false;
     }
   }
@@ -528,8 +697,13 @@ template <typename R> static void gather(Ctx& c, int l, const std::vector<Node>&
       reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const int32_t*>(c.d_ia.p),
       reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
   launch_check("gather_kernel", xblocks * groups, threads, 0);
+  double2 kf = make_double2(1.0, 0.0);
+  if (c.kernel_version == 2) {  // deferred W-form scalars of both blocks
+    const double ar = c.kfinal[0][0], ai = c.kfinal[0][1], br = c.kfinal[1][0], bi = c.kfinal[1][1];
+    kf = make_double2(ar * br - ai * bi, ar * bi + ai * br);
+  }
   reduce_kernel<<<(unsigned)xblocks, threads, 0, c.stream>>>(
-      reinterpret_cast<const double2*>(c.d_partial.p), (int)groups, nreq,
+      reinterpret_cast<const double2*>(c.d_partial.p), (int)groups, nreq, kf,
       reinterpret_cast<double2*>(c.d_acc.p));
   launch_check("reduce_kernel", xblocks, threads, 0);
   c.st.n_gather_launches += 2;
@@ -756,6 +930,13 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "low_bits out of range");
       c.low_bits = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "reg_bits") {
+      if (value != 4 && value != 5) throw GsError(GS_ERR_ARG, "reg_bits must be 4 or 5");
+      c.reg_bits = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pass_kernel") {
+      if (value != 1 && value != 2) throw GsError(GS_ERR_ARG, "pass_kernel must be 1 or 2");
+      c.kernel_version = (int)value;
     } else if (k == "max_chunk") {
       if (value < 1) throw GsError(GS_ERR_ARG, "max_chunk must be positive");
       c.max_chunk = value;

@@ -206,17 +206,20 @@ gather_kernel(const void* A, const void* B, long long a_elems, long long b_elems
   partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
 }
 
-__global__ void __launch_bounds__(256)
-reduce_kernel(const double2* partial, int groups, long long n_req, double2* acc) {
+static __global__ void __launch_bounds__(256)
+reduce_kernel(const double2* partial, int groups, long long n_req, double2 k, double2* acc) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_req) return;
-  double2 s = acc[i];
+  double2 s = make_double2(0.0, 0.0);
   for (int g = 0; g < groups; ++g) {
     const double2 p = partial[(long long)g * n_req + i];
     s.x += p.x;
     s.y += p.y;
   }
-  acc[i] = s;
+  double2 a = acc[i];
+  a.x += k.x * s.x - k.y * s.y;
+  a.y += k.x * s.y + k.y * s.x;
+  acc[i] = a;
 }
 
 }  // namespace gs

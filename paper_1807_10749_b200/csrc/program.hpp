@@ -36,7 +36,15 @@ struct HostOp {
   int s0 = -1, s1 = -1;
   int64_t coef = 0;  // coefficient pool offset (non-cross)
   int cross = -1;    // cross gate index (digit-dependent coefficients)
+  int w = -1;        // W-form of a K_MAT1 (0 H, 1 X^1/2, 2 Y^1/2): u = s * W
+  double s_re = 1, s_im = 0;
   bool diag() const { return kind == K_DIAG1 || kind == K_DIAG2; }
+};
+
+// A stage of a pass: M tile bits held in registers and the ops applied there.
+struct StagePlan {
+  std::vector<int> rb;  // register bit i -> tile bit
+  std::vector<HostOp> ops;
 };
 
 struct PassPlan {
@@ -44,7 +52,11 @@ struct PassPlan {
   std::vector<int> lbits;       // tile bit -> state bit (ascending)
   std::vector<int> gbits;       // tile-id bit -> state bit (ascending)
   std::vector<HostOp> ops;      // ops applied in this pass, in order
-  int64_t dev_op_offset = 0;    // into the device op array
+  int64_t dev_op_offset = 0;    // into the device op array (v1 kernel)
+  std::vector<StagePlan> stages;
+  int M = 0;                    // register bits per stage
+  int64_t dev_stage_offset = 0; // into the device stage array
+  double store_scale = 1.0;     // power of two applied on store
 };
 
 struct Level {
@@ -135,6 +147,88 @@ inline std::vector<PassPlan> schedule_passes(const std::vector<HostOp>& ops, int
     p.ops = std::move(taken);
     out.push_back(std::move(p));
     remaining = std::move(deferred);
+  }
+  return out;
+}
+
+// Split one pass into register stages.  Each stage holds M tile bits in
+// registers; a non-diagonal op needs all its qubits there, a diagonal op can
+// run in any stage (its other bits are thread- or tile-uniform).  Stage 0
+// and the last stage keep tile bits 0..4 on the lanes (when the tile has room)
+// so the HBM load and store are warp-contiguous.
+inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M) {
+  const int k = pp.k;
+  std::vector<int> tile_of(64, -1);
+  for (int j = 0; j < k; ++j) tile_of[pp.lbits[j]] = j;
+  const int lane_low = (k - 5 >= M) ? 5 : 0;
+  std::vector<StagePlan> out;
+  std::vector<HostOp> remaining = pp.ops;
+  bool first = true;
+  while (!remaining.empty() || first) {
+    std::vector<char> in_r(k, 0);
+    int n_r = 0;
+    std::vector<char> blk_nd(k, 0), blk_d(k, 0);
+    std::vector<HostOp> taken, deferred;
+    auto allowed = [&](int j) { return j >= (first ? lane_low : 0); };
+    for (const HostOp& op : remaining) {
+      const int sb[2] = {op.s0, op.s1};
+      int tb[2] = {-1, -1};
+      for (int i = 0; i < 2; ++i)
+        if (sb[i] >= 0) tb[i] = tile_of[sb[i]];
+      bool nd_block = false, d_block = false;
+      for (int b : tb)
+        if (b >= 0) nd_block |= blk_nd[b], d_block |= blk_d[b];
+      if (op.diag()) {
+        if (nd_block) {
+          deferred.push_back(op);
+          for (int b : tb)
+            if (b >= 0) blk_d[b] = 1;
+        } else {
+          taken.push_back(op);
+        }
+        continue;
+      }
+      bool ok = !(nd_block || d_block);
+      if (ok) {
+        int need = 0;
+        for (int i = 0; i < 2; ++i) {
+          if (sb[i] < 0) continue;
+          const int b = tb[i];
+          if (b < 0) { ok = false; break; }  // dense op outside the tile: scheduler bug
+          if (!in_r[b]) { ++need; if (!allowed(b)) ok = false; }
+        }
+        ok = ok && (n_r + need <= M);
+      }
+      if (ok) {
+        for (int b : tb)
+          if (b >= 0 && !in_r[b]) in_r[b] = 1, ++n_r;
+        taken.push_back(op);
+      } else {
+        deferred.push_back(op);
+        for (int b : tb)
+          if (b >= 0) blk_nd[b] = 1;
+      }
+    }
+    if (taken.empty() && !first) throw GsError(-1, "stage scheduler made no progress");
+    for (int j = k - 1; j >= 0 && n_r < M; --j)
+      if (!in_r[j] && allowed(j)) in_r[j] = 1, ++n_r;
+    for (int j = k - 1; j >= 0 && n_r < M; --j)
+      if (!in_r[j]) in_r[j] = 1, ++n_r;
+    StagePlan sp;
+    for (int j = 0; j < k; ++j)
+      if (in_r[j]) sp.rb.push_back(j);
+    sp.ops = std::move(taken);
+    out.push_back(std::move(sp));
+    remaining = std::move(deferred);
+    first = false;
+  }
+  // the store stage must leave tile bits 0..4 on the lanes
+  bool low_in_r = false;
+  for (int j : out.back().rb) low_in_r |= (j < lane_low);
+  if (low_in_r) {
+    StagePlan sp;
+    for (int j = k - M; j < k; ++j) sp.rb.push_back(j);
+    out.push_back(std::move(sp));
   }
   return out;
 }
