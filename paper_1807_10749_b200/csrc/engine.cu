@@ -91,7 +91,7 @@ struct Node {
   int64_t key;      // prefix digits [0, min(e, x_p)) as a number
   int64_t bkey;     // branch digits [x_p, max(e, x_p)) as a number
   int64_t b0, b1;   // branch id range
-  int32_t digit;    // this level's digits (mixed radix), for the cross ops
+  uint64_t digit;   // this level's cross digits, 4 bits each (gate k_lo + j at bits 4j)
   int32_t parent;   // slot of the parent in the previous level's buffer
 };
 
@@ -125,9 +125,12 @@ struct Ctx {
   // program
   bool have_prog = false;
   Program prog;
-  DevBuf d_ops, d_coef, d_xtable, d_pops, d_pstages;
+  DevBuf d_ops, d_coef, d_xtable, d_prims, d_pstages, d_params, d_pxtable;
   std::vector<DevOp> host_devops;
-  std::vector<POp> host_pops;
+  std::vector<PPrim> host_prims;
+  std::vector<double> host_params;   // 4 per param: rs, t, sn, mode
+  std::vector<int32_t> host_pxtable;
+  std::vector<int> pxbase[2];        // per cross gate and side: pxtable base
   std::vector<PStage> host_pstages;
   double kfinal[2][2] = {{1, 0}, {1, 0}};  // per block: true = stored * K
   int kernel_version = 2;
@@ -303,6 +306,167 @@ static void build_program(Ctx& c, int qa, int qb, int n_ops, const int32_t* kind
   c.prog = std::move(p);
 }
 
+// diagonal factor d -> {rs, t, sn, mode}: d = rs * e^{i theta}, |theta| <= pi/2
+static int add_param(Ctx& c, double re, double im) {
+  double m = std::sqrt(re * re + im * im);
+  double rs = m, cs = 1, sn = 0;
+  if (m > 0) cs = re / m, sn = im / m;
+  if (std::fabs(m - 1.0) < 1e-12) rs = 1.0;
+  if (cs < 0) cs = -cs, sn = -sn, rs = -rs;
+  if (std::fabs(sn) < 1e-15) sn = 0;
+  const int mode = (rs != 1.0 ? 1 : 0) | (sn != 0 ? 2 : 0);
+  const int at = (int)(c.host_params.size() / 4);
+  c.host_params.insert(c.host_params.end(), {rs, sn / (1.0 + cs), sn, (double)mode});
+  return at;
+}
+
+static bool is_identity(const double* z) { return z[0] == 1.0 && z[1] == 0.0; }
+
+// lower one scheduled op into jump-table primitives (pass_types.h PrimCode)
+static void emit_prims(Ctx& c, int side, const Level& L, const HostOp& op, const std::vector<int>& tpos,
+                       const std::vector<int>& rpos) {
+  const Program& p = c.prog;
+  struct Bit { int where, idx; };
+  auto loc = [&](int sb) -> Bit {
+    const int t = tpos[sb];
+    if (t >= 0 && rpos[t] >= 0) return {B_REG, rpos[t]};
+    if (t >= 0) return {B_THREAD, t};
+    return {B_TILE, sb};
+  };
+  auto prim = [&](int code) {
+    PPrim q{};
+    q.code = (uint8_t)code;
+    q.ub_where = 255;
+    return q;
+  };
+  auto set_ua = [](PPrim& q, Bit b) { q.ua_where = (uint8_t)b.where, q.ua_idx = (uint8_t)b.idx; };
+  auto set_ub = [](PPrim& q, Bit b) { q.ub_where = (uint8_t)b.where, q.ub_idx = (uint8_t)b.idx; };
+  const double* cf = p.coef.data();
+  if (op.cross >= 0) {
+    const int k = op.cross;
+    const Bit b = loc(op.s0);
+    // per-digit table: diag sides -> [lo param, hi param]; dense sides -> coef offset
+    if (c.pxbase[side][k] < 0) {
+      c.pxbase[side][k] = (int)c.host_pxtable.size();
+      for (int d = 0; d < p.radix[k]; ++d) {
+        const int32_t off = p.xtable[p.xtab[side][k] + d];
+        if (p.xdiag[side][k]) {
+          const int lo = add_param(c, cf[2 * off], cf[2 * off + 1]);
+          add_param(c, cf[2 * off + 2], cf[2 * off + 3]);
+          c.host_pxtable.push_back(lo);
+        } else {
+          c.host_pxtable.push_back(off);
+        }
+      }
+    }
+    const int xk = k - L.k_lo;
+    if (xk >= 16 || p.radix[k] > 16) throw GsError(GS_ERR_ARG, "level digits exceed the packed nibble format");
+    auto crossify = [&](PPrim q, int xsub) {
+      q.flags = 1;
+      q.param = c.pxbase[side][k];
+      q.xk = (uint8_t)xk;
+      q.xsub = (int16_t)xsub;
+      c.host_prims.push_back(q);
+    };
+    if (!p.xdiag[side][k]) {
+      PPrim q = prim(C_M1);
+      q.r0 = (uint8_t)b.idx;
+      crossify(q, 0);
+    } else if (b.where == B_REG) {
+      crossify(prim(C_DH + 0 * 5 + b.idx), 0);
+      crossify(prim(C_DH + 1 * 5 + b.idx), 1);
+    } else {
+      PPrim q = prim(C_DSEL);
+      set_ua(q, b);
+      crossify(q, 0);
+    }
+    return;
+  }
+  const double* u = cf + 2 * op.coef;
+  switch (op.kind) {
+    case K_MAT1: {
+      const Bit b = loc(op.s0);
+      PPrim q = prim(op.w >= 0 ? C_W + op.w * 5 + b.idx : C_M1);
+      q.r0 = (uint8_t)b.idx;
+      q.param = (int32_t)op.coef;
+      c.host_prims.push_back(q);
+      break;
+    }
+    case K_DIAG1: {
+      const Bit b = loc(op.s0);
+      if (b.where == B_REG) {
+        for (int h = 0; h < 2; ++h) {
+          if (is_identity(u + 2 * h)) continue;
+          PPrim q = prim(C_DH + h * 5 + b.idx);
+          q.param = add_param(c, u[2 * h], u[2 * h + 1]);
+          c.host_prims.push_back(q);
+        }
+      } else if (!(is_identity(u) && is_identity(u + 2))) {
+        PPrim q = prim(C_DSEL);
+        set_ua(q, b);
+        q.param = add_param(c, u[0], u[1]);
+        add_param(c, u[2], u[3]);
+        c.host_prims.push_back(q);
+      }
+      break;
+    }
+    case K_DIAG2: {
+      const Bit ba = loc(op.s0), bb = loc(op.s1);
+      auto dz = [&](int xa, int xb) { return u + 2 * (2 * xa + xb); };
+      if (ba.where == B_REG && bb.where == B_REG) {
+        const int lo = std::min(ba.idx, bb.idx), hi = std::max(ba.idx, bb.idx);
+        int pair = 0;
+        for (int i = 0; i < lo; ++i) pair += 4 - i;
+        pair += hi - lo - 1;
+        for (int xa = 0; xa < 2; ++xa)
+          for (int xb = 0; xb < 2; ++xb) {
+            const double* z = dz(xa, xb);
+            if (is_identity(z)) continue;
+            const int xl = ba.idx < bb.idx ? xa : xb, xh = ba.idx < bb.idx ? xb : xa;
+            PPrim q = prim(C_DQ + pair * 4 + 2 * xl + xh);
+            q.param = add_param(c, z[0], z[1]);
+            c.host_prims.push_back(q);
+          }
+      } else if (ba.where == B_REG || bb.where == B_REG) {
+        const bool a_reg = ba.where == B_REG;
+        const Bit r = a_reg ? ba : bb, un = a_reg ? bb : ba;
+        for (int h = 0; h < 2; ++h) {
+          const double* z0 = a_reg ? dz(h, 0) : dz(0, h);
+          const double* z1 = a_reg ? dz(h, 1) : dz(1, h);
+          if (is_identity(z0) && is_identity(z1)) continue;
+          PPrim q = prim(C_DHSEL + h * 5 + r.idx);
+          set_ua(q, un);
+          q.param = add_param(c, z0[0], z0[1]);
+          add_param(c, z1[0], z1[1]);
+          c.host_prims.push_back(q);
+        }
+      } else {
+        bool ident = true;
+        for (int i = 0; i < 4; ++i) ident &= is_identity(u + 2 * i);
+        if (!ident) {
+          PPrim q = prim(C_DSEL);
+          set_ua(q, ba);
+          set_ub(q, bb);
+          q.param = add_param(c, u[0], u[1]);
+          for (int i = 1; i < 4; ++i) add_param(c, u[2 * i], u[2 * i + 1]);
+          c.host_prims.push_back(q);
+        }
+      }
+      break;
+    }
+    default: {  // K_MAT2
+      const Bit ba = loc(op.s0), bb = loc(op.s1);
+      if (ba.where != B_REG || bb.where != B_REG)
+        throw GsError(GS_ERR_ARG, "stage scheduler placed a dense op outside the registers");
+      PPrim q = prim(C_M2);
+      q.r0 = (uint8_t)ba.idx;
+      q.r1 = (uint8_t)bb.idx;
+      q.param = (int32_t)op.coef;
+      c.host_prims.push_back(q);
+    }
+  }
+}
+
 static void schedule_program(Ctx& c) {
   Program& p = c.prog;
   c.host_devops.clear();
@@ -322,9 +486,7 @@ static void schedule_program(Ctx& c) {
           d.coef = (int32_t)op.coef;
           if (op.cross >= 0) {
             d.xtab = p.xtab[side][op.cross];
-            int64_t stride = 1;
-            for (int k = op.cross + 1; k < L.k_hi; ++k) stride *= p.radix[k];
-            d.xstride = (int32_t)stride;
+            d.xstride = op.cross - L.k_lo;  // nibble of the packed node digits
             d.xradix = p.radix[op.cross];
           }
           auto enc = [&](int s, int32_t& b, int32_t& g) {
@@ -347,7 +509,11 @@ static void schedule_program(Ctx& c) {
     }
   }
   // v2: register stages per pass, W scalars folded into one constant per block
-  c.host_pops.clear();
+  c.host_prims.clear();
+  c.host_params.clear();
+  c.host_pxtable.clear();
+  c.pxbase[0].assign(p.n_cross, -1);
+  c.pxbase[1].assign(p.n_cross, -1);
   c.host_pstages.clear();
   for (int side = 0; side < 2; ++side) {
     double kre = 1.0, kim = 0.0;  // true amplitude = stored * K
@@ -358,6 +524,9 @@ static void schedule_program(Ctx& c) {
         // the tile) keep the v1 shared-memory kernel
         pp.M = (c.precision == GS_C64 && pp.k >= 5 && c.reg_bits != 4) ? 5 : (pp.k >= 4 ? 4 : 0);
         if (pp.M == 0) continue;
+        // tile = k state bits + slot bits batching small states, up to 2^13 (c64) /
+        // 2^12 (c128) amplitudes and 256 threads
+        pp.K = std::max(pp.k, std::min(c.kmax(), pp.M + 8));
         pp.stages = schedule_stages(pp, pp.M);
         pp.dev_stage_offset = (int64_t)c.host_pstages.size();
         std::vector<int> tpos(p.q[side], -1);
@@ -366,46 +535,42 @@ static void schedule_program(Ctx& c) {
           PStage ps{};
           std::vector<int> rpos(pp.k, -1);
           for (int i = 0; i < (int)sp.rb.size(); ++i) ps.rb[i] = (int8_t)sp.rb[i], rpos[sp.rb[i]] = i;
-          ps.op_begin = (int32_t)c.host_pops.size();
+          // thread-bit order over the tile bits (state bits then slot bits up to
+          // the kernel's K); lanes are thread bits 0..4.  HBM stages keep the
+          // lowest tile bits on the lanes; shared-memory-only stages pick lanes
+          // whose swizzle classes are distinct (conflict-free exchanges).
+          {
+            const size_t si = &sp - &pp.stages[0];
+            const bool hbm_stage = (si == 0) || (si + 1 == pp.stages.size());
+            std::vector<int> tbits;
+            for (int j = 0; j < pp.K; ++j)
+              if (j >= pp.k || rpos[j] < 0) tbits.push_back(j);
+            if (!hbm_stage) {
+              const int nclass = (c.precision == GS_C64) ? 4 : 3;
+              std::vector<int> lanes, rest;
+              std::vector<char> used_class(nclass, 0);
+              for (int j : tbits) {
+                if ((int)lanes.size() < nclass && !used_class[j % nclass]) {
+                  used_class[j % nclass] = 1;
+                  lanes.push_back(j);
+                } else {
+                  rest.push_back(j);
+                }
+              }
+              tbits = lanes;
+              tbits.insert(tbits.end(), rest.begin(), rest.end());
+            }
+            for (int j = 0; j < (int)tbits.size() && j < 16; ++j) ps.tb[j] = (int8_t)tbits[j];
+          }
+          ps.op_begin = (int32_t)c.host_prims.size();
           for (const HostOp& op : sp.ops) {
-            POp d{};
-            d.xtab = -1;
-            d.xstride = 1;
-            d.xradix = 1;
-            d.coef = (int32_t)op.coef;
-            d.w = (int8_t)op.w;
-            if (op.cross >= 0) {
-              d.xtab = p.xtab[side][op.cross];
-              int64_t stride = 1;
-              for (int k = op.cross + 1; k < L.k_hi; ++k) stride *= p.radix[k];
-              d.xstride = (int32_t)stride;
-              d.xradix = p.radix[op.cross];
-            }
-            auto enc = [&](int sb, int8_t& where, int8_t& idx) {
-              if (sb < 0) { where = B_REG; idx = 0; return; }
-              const int t = tpos[sb];
-              if (t >= 0 && rpos[t] >= 0) { where = B_REG; idx = (int8_t)rpos[t]; }
-              else if (t >= 0) { where = B_THREAD; idx = (int8_t)t; }
-              else { where = B_TILE; idx = (int8_t)sb; }
-            };
-            enc(op.s0, d.where0, d.idx0);
-            enc(op.s1, d.where1, d.idx1);
-            switch (op.kind) {
-              case K_MAT1: d.type = (op.w >= 0) ? P_W : P_M1; break;
-              case K_DIAG1: d.type = P_D1; break;
-              case K_DIAG2: d.type = P_D2; break;
-              default: d.type = P_M2; break;
-            }
-            if ((d.type == P_W || d.type == P_M1 || d.type == P_M2) &&
-                (d.where0 != B_REG || (d.type == P_M2 && d.where1 != B_REG)))
-              throw GsError(GS_ERR_ARG, "stage scheduler placed a dense op outside the registers");
+            emit_prims(c, side, L, op, tpos, rpos);
             if (op.w >= 0) {  // K *= s
               const double r = kre * op.s_re - kim * op.s_im, i = kre * op.s_im + kim * op.s_re;
               kre = r, kim = i;
             }
-            c.host_pops.push_back(d);
           }
-          ps.op_end = (int32_t)c.host_pops.size();
+          ps.op_end = (int32_t)c.host_prims.size();
           c.host_pstages.push_back(ps);
         }
         // power-of-two rescale on store keeps |stored| ~ |true amplitude|
@@ -440,8 +605,15 @@ template <typename T> static void upload(Ctx& c, DevBuf& b, const std::vector<T>
 static void upload_program(Ctx& c) {
   if (c.host_only) return;
   upload(c, c.d_ops, c.host_devops);
-  upload(c, c.d_pops, c.host_pops);
+  upload(c, c.d_prims, c.host_prims);
   upload(c, c.d_pstages, c.host_pstages);
+  upload(c, c.d_pxtable, c.host_pxtable);
+  if (c.precision == GS_C64) {
+    std::vector<float> f(c.host_params.begin(), c.host_params.end());
+    upload(c, c.d_params, f);
+  } else {
+    upload(c, c.d_params, c.host_params);
+  }
   upload(c, c.d_xtable, c.prog.xtable);
   if (c.precision == GS_C64) {
     std::vector<float> f(c.prog.coef.begin(), c.prog.coef.end());
@@ -458,6 +630,17 @@ static int64_t level_fanout(const Program& p, int l) {
   int64_t f = 1;
   for (int k = p.levels[l].k_lo; k < p.levels[l].k_hi; ++k) f *= p.radix[k];
   return f;
+}
+
+// mixed-radix level digit value -> packed nibbles (gate k_lo + j at bits 4j)
+static uint64_t pack_level_digits(const Program& p, int l, int64_t v) {
+  const Level& L = p.levels[l];
+  uint64_t out = 0;
+  for (int k = L.k_hi - 1; k >= L.k_lo; --k) {
+    out |= (uint64_t)(v % p.radix[k]) << (4 * (k - L.k_lo));
+    v /= p.radix[k];
+  }
+  return out;
 }
 
 // children of `parents` (level l) at level l+1, appended to `out` in leaf order
@@ -477,7 +660,7 @@ static void enumerate_children(Ctx& c, int l, const Node* parents, int64_t n_par
         const int64_t ck = pre[i] / S;
         const int64_t lim = (ck + 1) * S;  // first prefix value of the next child
         const int64_t j = std::lower_bound(pre.begin() + i, pre.begin() + N.i1, lim) - pre.begin();
-        Node ch{i, j, ck, 0, N.b0, N.b1, (int32_t)(ck - N.key * F), (int32_t)s};
+        Node ch{i, j, ck, 0, N.b0, N.b1, pack_level_digits(p, l + 1, ck - N.key * F), (int32_t)s};
         out.push_back(ch);
         i = j;
       }
@@ -493,7 +676,7 @@ static void enumerate_children(Ctx& c, int l, const Node* parents, int64_t n_par
         for (int64_t cb = lo; cb <= hi; ++cb) {
           const int64_t b0 = std::max(cb * Sb, N.b0), b1 = std::min((cb + 1) * Sb, N.b1);
           if (b0 >= b1) continue;
-          Node ch{i, i + 1, pre[i], cb, b0, b1, (int32_t)(vp * Fb + (cb - N.bkey * Fb)), (int32_t)s};
+          Node ch{i, i + 1, pre[i], cb, b0, b1, pack_level_digits(p, l + 1, vp * Fb + (cb - N.bkey * Fb)), (int32_t)s};
           out.push_back(ch);
         }
       }
@@ -514,14 +697,14 @@ static void launch_check(const char* what, int64_t blocks, int threads, size_t s
 
 template <typename R>
 static void launch_pass(Ctx& c, int side, const PassPlan& pp, const void* src, void* dst,
-                        const int32_t* parent, const int32_t* digit, int64_t n_states,
+                        const int32_t* parent, const uint64_t* digit, int64_t n_states,
                         bool init_zero) {
   const int q = c.prog.q[side];
   PassArgs a{};
   a.src = src;
   a.dst = dst;
   a.parent = parent;
-  a.digit = digit;
+  a.digit = reinterpret_cast<const unsigned long long*>(digit);
   a.ops = reinterpret_cast<const DevOp*>(c.d_ops.p) + pp.dev_op_offset;
   a.coefs = c.d_coef.p;
   a.xtable = reinterpret_cast<const int32_t*>(c.d_xtable.p);
@@ -568,15 +751,17 @@ static void launch_pass2_m(Ctx& c, const Pass2Args& a, int64_t blocks, int threa
 
 template <typename R>
 static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, void* dst,
-                         const int32_t* parent, const int32_t* digit, int64_t n_states,
+                         const int32_t* parent, const uint64_t* digit, int64_t n_states,
                          bool init_zero) {
   const int q = c.prog.q[side];
   Pass2Args a{};
   a.src = src;
   a.dst = dst;
   a.parent = parent;
-  a.digit = digit;
-  a.ops = reinterpret_cast<const POp*>(c.d_pops.p);
+  a.digits = reinterpret_cast<const unsigned long long*>(digit);
+  a.prims = reinterpret_cast<const PPrim*>(c.d_prims.p);
+  a.params = c.d_params.p;
+  a.pxtable = reinterpret_cast<const int32_t*>(c.d_pxtable.p);
   a.stages = reinterpret_cast<const PStage*>(c.d_pstages.p) + pp.dev_stage_offset;
   a.coefs = c.d_coef.p;
   a.xtable = reinterpret_cast<const int32_t*>(c.d_xtable.p);
@@ -585,9 +770,8 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
   a.store_scale = pp.store_scale;
   a.n_stages = (int)pp.stages.size();
   a.kq = pp.k;
-  const int kcap = std::min(c.kmax(), pp.M + 8);
-  const int slots = std::max(0, std::min(kcap - pp.k, ceil_log2(n_states)));
-  a.K = pp.k + slots;
+  const int slots = pp.K - pp.k;
+  a.K = pp.K;
   int cc = 0;
   while (cc < pp.k && pp.lbits[cc] == cc) ++cc;
   a.c = std::min(cc, 10);
@@ -597,7 +781,7 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
   for (int j = 0; j < pp.k; ++j) a.lbits[j] = pp.lbits[j];
   for (int j = 0; j < (int)pp.gbits.size(); ++j) a.gbits[j] = pp.gbits[j];
   const int threads = 1 << (a.K - pp.M);
-  const size_t smem = ((size_t)1 << a.K) * c.esize() + (size_t)a.n_hi * sizeof(int);
+  const size_t smem = ((size_t)1 << a.K) * c.esize();
   const int64_t groups = (n_states + (1LL << slots) - 1) >> slots;
   const int64_t blocks = groups << a.tiles_log;
   if (blocks > INT32_MAX) throw GsError(GS_ERR_ARG, "grid too large");
@@ -640,7 +824,7 @@ struct Timer {
 template <typename R>
 static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const void* src_b,
                              void* dst_a, void* dst_b, const int32_t* parent,
-                             const int32_t* digit, bool root) {
+                             const uint64_t* digit, bool root) {
   Timer t(c, &c.st.ms_pass);
   const Level& L = c.prog.levels[l];
   const void* srcs[2] = {src_a, src_b};
@@ -727,17 +911,18 @@ template <typename R> static void descend(Ctx& c, int l, const std::vector<Node>
     if (!c.host_only) {
       PinnedBuf& stg = c.lvl_stage[l + 1];
       cudaEventSynchronize(c.lvl_event[l + 1]);
-      int32_t* h = reinterpret_cast<int32_t*>(stg.p);
-      for (int64_t j = 0; j < n; ++j) h[j] = chunk[j].parent, h[n + j] = chunk[j].digit;
-      CK(cudaMemcpyAsync(c.lvl_parent[l + 1].p, h, n * 4, cudaMemcpyHostToDevice, c.stream));
-      CK(cudaMemcpyAsync(c.lvl_digit[l + 1].p, h + n, n * 4, cudaMemcpyHostToDevice, c.stream));
-      c.st.h2d_bytes += 8.0 * n;
+      uint64_t* hd = reinterpret_cast<uint64_t*>(stg.p);
+      int32_t* hp = reinterpret_cast<int32_t*>(hd + n);
+      for (int64_t j = 0; j < n; ++j) hd[j] = chunk[j].digit, hp[j] = chunk[j].parent;
+      CK(cudaMemcpyAsync(c.lvl_digit[l + 1].p, hd, n * 8, cudaMemcpyHostToDevice, c.stream));
+      CK(cudaMemcpyAsync(c.lvl_parent[l + 1].p, hp, n * 4, cudaMemcpyHostToDevice, c.stream));
+      c.st.h2d_bytes += 12.0 * n;
       CK(cudaEventRecord(c.lvl_event[l + 1], c.stream));
     }
     auto at = [](std::vector<DevBuf>& v, int i) -> void* { return i < (int)v.size() ? v[i].p : nullptr; };
     run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
                         at(c.lvl_b, l + 1), reinterpret_cast<const int32_t*>(at(c.lvl_parent, l + 1)),
-                        reinterpret_cast<const int32_t*>(at(c.lvl_digit, l + 1)), false);
+                        reinterpret_cast<const uint64_t*>(at(c.lvl_digit, l + 1)), false);
     (void)ea;
     (void)eb;
     descend<R>(c, l + 1, chunk);
@@ -795,8 +980,8 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
     c.lvl_a[l].ensure((size_t)c.cap[l] * ((size_t)1 << p.q[0]) * c.esize());
     c.lvl_b[l].ensure((size_t)c.cap[l] * ((size_t)1 << p.q[1]) * c.esize());
     c.lvl_parent[l].ensure(c.cap[l] * 4 + 16);
-    c.lvl_digit[l].ensure(c.cap[l] * 4 + 16);
-    c.lvl_stage[l].ensure(c.cap[l] * 8 + 16);
+    c.lvl_digit[l].ensure(c.cap[l] * 8 + 16);
+    c.lvl_stage[l].ensure(c.cap[l] * 12 + 16);
   }
   if (!c.weights_event) CK(cudaEventCreateWithFlags(&c.weights_event, cudaEventDisableTiming));
 }

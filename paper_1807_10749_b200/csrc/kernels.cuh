@@ -30,7 +30,7 @@ struct DevOp {
   int32_t g0, g1;  // 1 = bit is outside the tile (fixed per tile)
   int32_t coef;    // coefficient offset (non-cross ops)
   int32_t xtab;    // >= 0: cross op; coef = xtable[xtab + digit]
-  int32_t xstride; // digit = (node_digit / xstride) % xradix
+  int32_t xstride; // digit = (node_digits >> 4*xstride) & 15
   int32_t xradix;
   int32_t pad;
 };
@@ -57,7 +57,7 @@ struct PassArgs {
   const void* src;         // parent states (first pass) or dst (in place)
   void* dst;               // child states
   const int32_t* parent;   // parent slot per child state, nullptr = identity
-  const int32_t* digit;    // node digit per child state (cross ops), may be null
+  const unsigned long long* digit;  // packed 4-bit node digits per child state, may be null
   const DevOp* ops;
   const void* coefs;
   const int32_t* xtable;
@@ -113,11 +113,11 @@ __global__ void __launch_bounds__(256) gate_pass_kernel(PassArgs a) {
   __syncthreads();
 
   const V* coefs = reinterpret_cast<const V*>(a.coefs);
-  const int node_digit = a.digit ? a.digit[state] : 0;
+  const unsigned long long node_digit = a.digit ? a.digit[state] : 0ull;
   for (int oi = 0; oi < a.n_ops; ++oi) {
     const DevOp op = a.ops[oi];
     int cofs = op.coef;
-    if (op.xtab >= 0) cofs = a.xtable[op.xtab + (node_digit / op.xstride) % op.xradix];
+    if (op.xtab >= 0) cofs = a.xtable[op.xtab + (int)((node_digit >> (4 * op.xstride)) & 15)];
     const V* u = coefs + cofs;
     if (op.type == D_MAT1) {
       const V u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];

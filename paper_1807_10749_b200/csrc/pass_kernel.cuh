@@ -26,86 +26,43 @@
 
 namespace gs {
 
-template <typename V> __device__ __forceinline__ bool is_one(V d) { return d.x == 1 && d.y == 0; }
-template <typename V> __device__ __forceinline__ bool is_zero(V d) { return d.x == 0 && d.y == 0; }
-template <typename V> __device__ __forceinline__ bool is_mone(V d) { return d.x == -1 && d.y == 0; }
+// Every common op below updates its registers strictly in place (no value
+// outlives the op in a temporary).  With runtime dispatch over many inlined
+// op bodies, any temporary left holding a result forces the register
+// allocator to copy the whole 2^M-amplitude array at the op-loop header.
 
-// 0 identity, 1 zero, 2 negate, 3 general
-template <typename V> __device__ __forceinline__ int dkind(V d) {
-  return is_one(d) ? 0 : is_zero(d) ? 1 : is_mone(d) ? 2 : 3;
+// x *= e^{i theta} as three in-place shears (Paeth): t = tan(theta/2),
+// sn = sin(theta).  The host folds any angle beyond +-pi/2 into the sign of the
+// real scale (add_param), so tan stays bounded.
+template <typename V, typename T>
+__device__ __forceinline__ void rot_inplace(V& x, T t, T sn) {
+  x.x = fma(-t, x.y, x.x);
+  x.y = fma(sn, x.x, x.y);
+  x.x = fma(-t, x.y, x.x);
 }
 
-template <typename V> __device__ __forceinline__ V dapply(V x, V d, int kind) {
-  if (kind == 1) { x.x = 0; x.y = 0; return x; }
-  if (kind == 2) { x.x = -x.x; x.y = -x.y; return x; }
-  return cmul(x, d);
-}
-
-template <int M, typename V> __device__ __forceinline__ void scale_all(V (&v)[1 << M], V d) {
-  const int kind = dkind(d);
-  if (kind == 0) return;
-#pragma unroll
-  for (int e = 0; e < (1 << M); ++e) v[e] = dapply(v[e], d, kind);
-}
-
-// diag(d0, d1) on register bit B
-template <int M, int B, typename V>
-__device__ __forceinline__ void d1_reg(V (&v)[1 << M], V d0, V d1) {
-  const int k0 = dkind(d0), k1 = dkind(d1);
-  if (k0)
-#pragma unroll
-    for (int e = 0; e < (1 << M); ++e)
-      if (!((e >> B) & 1)) v[e] = dapply(v[e], d0, k0);
-  if (k1)
-#pragma unroll
-    for (int e = 0; e < (1 << M); ++e)
-      if ((e >> B) & 1) v[e] = dapply(v[e], d1, k1);
-}
-
-// diag on register bits (A = qa, B = qb): amplitude (a, b) times d[2a + b]
-template <int M, int A, int B, typename V>
-__device__ __forceinline__ void d2_reg(V (&v)[1 << M], const V* d) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const V dq = d[q];
-    const int kind = dkind(dq);
-    if (!kind) continue;
-#pragma unroll
-    for (int e = 0; e < (1 << M); ++e)
-      if ((((e >> A) & 1) << 1 | ((e >> B) & 1)) == q) v[e] = dapply(v[e], dq, kind);
-  }
-}
-
-template <int M, int B, typename V>
-__device__ __forceinline__ void m1_reg(V (&v)[1 << M], V u00, V u01, V u10, V u11) {
-#pragma unroll
-  for (int e = 0; e < (1 << M); ++e) {
-    if ((e >> B) & 1) continue;
-    const V x0 = v[e], x1 = v[e | (1 << B)];
-    v[e] = cmad2(u00, x0, u01, x1);
-    v[e | (1 << B)] = cmad2(u10, x0, u11, x1);
-  }
-}
-
-// W-forms: H = [[1,1],[1,-1]], X = [[1,-i],[-i,1]], Y = [[1,-1],[1,1]]
+// W-forms, in place: H = [[1,1],[1,-1]], X = [[1,-i],[-i,1]], Y = [[1,-1],[1,1]].
+// The second output is recovered from the first with one FMA
+// (x0 - x1 = (x0 + x1) - 2 x1), so no temporary survives the op.
 template <int M, int B, int W, typename V> __device__ __forceinline__ void w_reg(V (&v)[1 << M]) {
+  using T = decltype(v[0].x);
 #pragma unroll
   for (int e = 0; e < (1 << M); ++e) {
     if ((e >> B) & 1) continue;
-    const V x0 = v[e], x1 = v[e | (1 << B)];
-    V y0, y1;
-    if (W == 0) {
-      y0.x = x0.x + x1.x; y0.y = x0.y + x1.y;
-      y1.x = x0.x - x1.x; y1.y = x0.y - x1.y;
-    } else if (W == 1) {
-      y0.x = x0.x + x1.y; y0.y = x0.y - x1.x;
-      y1.x = x1.x + x0.y; y1.y = x1.y - x0.x;
-    } else {
-      y0.x = x0.x - x1.x; y0.y = x0.y - x1.y;
-      y1.x = x0.x + x1.x; y1.y = x0.y + x1.y;
+    V& x0 = v[e];
+    V& x1 = v[e | (1 << B)];
+    if (W == 0) {         // y0 = x0 + x1, y1 = y0 - 2 x1
+      x0.x = x0.x + x1.x; x0.y = x0.y + x1.y;
+      x1.x = fma(T(-2), x1.x, x0.x); x1.y = fma(T(-2), x1.y, x0.y);
+    } else if (W == 1) {  // y0 = x0 - i x1, y1 = x1 - i x0
+      x0.x = x0.x + x1.y;                 // y0.re = x0.re + x1.im
+      x0.y = x0.y - x1.x;                 // y0.im = x0.im - x1.re
+      x1.x = fma(T(2), x1.x, x0.y);       // y1.re = x1.re + x0.im = 2 x1.re + y0.im
+      x1.y = fma(T(2), x1.y, -x0.x);      // y1.im = x1.im - x0.re = 2 x1.im - y0.re
+    } else {              // y0 = x0 - x1, y1 = y0 + 2 x1
+      x0.x = x0.x - x1.x; x0.y = x0.y - x1.y;
+      x1.x = fma(T(2), x1.x, x0.x); x1.y = fma(T(2), x1.y, x0.y);
     }
-    v[e] = y0;
-    v[e | (1 << B)] = y1;
   }
 }
 
@@ -122,291 +79,310 @@ __device__ __forceinline__ double2 ld_coef(const double2* p) {
   return r;
 }
 
-template <int M, int A, int B, typename V>
-__device__ __forceinline__ void m2_reg(V (&v)[1 << M], const V* u) {
-#pragma unroll
-  for (int e = 0; e < (1 << M); ++e) {
-    if (((e >> A) & 1) || ((e >> B) & 1)) continue;
-    V x[4], y[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) x[s] = v[e | ((s >> 1) << A) | ((s & 1) << B)];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      y[r].x = 0;
-      y[r].y = 0;
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const V w = ld_coef(u + 4 * r + s);
-        y[r].x += w.x * x[s].x - w.y * x[s].y;
-        y[r].y += w.x * x[s].y + w.y * x[s].x;
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < 4; ++s) v[e | ((s >> 1) << A) | ((s & 1) << B)] = y[s];
-  }
-}
 
-template <int M, int A, int B, typename V> __device__ __forceinline__ void d2_chk(V (&v)[1 << M], const V* d) {
-  if constexpr (A != B && A < M && B < M) d2_reg<M, A, B>(v, d);
-}
-template <int M, int A, int B, typename V> __device__ __forceinline__ void m2_chk(V (&v)[1 << M], const V* u) {
-  if constexpr (A != B && A < M && B < M) m2_reg<M, A, B>(v, u);
-}
 
-// runtime register-bit -> template dispatch
-#define GS_CASE1(M, B, CALL) \
-  case B:                    \
-    if constexpr (B < M) { CALL; } break;
-
-template <int M, typename V> __device__ __forceinline__ void d1_dispatch(V (&v)[1 << M], int r, V d0, V d1) {
-  switch (r) {
-    GS_CASE1(M, 0, (d1_reg<M, 0>(v, d0, d1)))
-    GS_CASE1(M, 1, (d1_reg<M, 1>(v, d0, d1)))
-    GS_CASE1(M, 2, (d1_reg<M, 2>(v, d0, d1)))
-    GS_CASE1(M, 3, (d1_reg<M, 3>(v, d0, d1)))
-    GS_CASE1(M, 4, (d1_reg<M, 4>(v, d0, d1)))
-  }
-}
-
-template <int M, typename V> __device__ __forceinline__ void m1_dispatch(V (&v)[1 << M], int r, const V* u) {
+// Dense 2x2 / 4x4 ops cannot be done in place; they run out of line on a
+// local copy of the registers so the hot in-place paths keep a fixed register
+// assignment (see the note above dkind).
+template <int M, typename V> __device__ __noinline__ void m1_mem(V* w, int r, const V* u) {
   const V u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
-  switch (r) {
-    GS_CASE1(M, 0, (m1_reg<M, 0>(v, u00, u01, u10, u11)))
-    GS_CASE1(M, 1, (m1_reg<M, 1>(v, u00, u01, u10, u11)))
-    GS_CASE1(M, 2, (m1_reg<M, 2>(v, u00, u01, u10, u11)))
-    GS_CASE1(M, 3, (m1_reg<M, 3>(v, u00, u01, u10, u11)))
-    GS_CASE1(M, 4, (m1_reg<M, 4>(v, u00, u01, u10, u11)))
+  for (int e = 0; e < (1 << M); ++e) {
+    if ((e >> r) & 1) continue;
+    const V x0 = w[e], x1 = w[e | (1 << r)];
+    w[e] = cmad2(u00, x0, u01, x1);
+    w[e | (1 << r)] = cmad2(u10, x0, u11, x1);
   }
 }
 
-template <int M, int W, typename V> __device__ __forceinline__ void w_dispatch_r(V (&v)[1 << M], int r) {
-  switch (r) {
-    GS_CASE1(M, 0, (w_reg<M, 0, W>(v)))
-    GS_CASE1(M, 1, (w_reg<M, 1, W>(v)))
-    GS_CASE1(M, 2, (w_reg<M, 2, W>(v)))
-    GS_CASE1(M, 3, (w_reg<M, 3, W>(v)))
-    GS_CASE1(M, 4, (w_reg<M, 4, W>(v)))
+template <int M, typename V> __device__ __noinline__ void m2_mem(V* w, int a, int b, const V* u) {
+  for (int e = 0; e < (1 << M); ++e) {
+    if (((e >> a) & 1) || ((e >> b) & 1)) continue;
+    V x[4];
+    for (int s = 0; s < 4; ++s) x[s] = w[e | ((s >> 1) << a) | ((s & 1) << b)];
+    for (int r = 0; r < 4; ++r) {
+      V y;
+      y.x = 0;
+      y.y = 0;
+      for (int s = 0; s < 4; ++s) {
+        const V c = u[4 * r + s];
+        y.x += c.x * x[s].x - c.y * x[s].y;
+        y.y += c.x * x[s].y + c.y * x[s].x;
+      }
+      w[e | ((r >> 1) << a) | ((r & 1) << b)] = y;
+    }
   }
 }
 
-template <int M, typename V> __device__ __forceinline__ void w_dispatch(V (&v)[1 << M], int w, int r) {
-  if (w == 0) w_dispatch_r<M, 0>(v, r);
-  else if (w == 1) w_dispatch_r<M, 1>(v, r);
-  else w_dispatch_r<M, 2>(v, r);
+template <int M, typename V> __device__ __forceinline__ void m1_outofline(V (&v)[1 << M], int r, const V* u) {
+  V w[1 << M];
+#pragma unroll
+  for (int e = 0; e < (1 << M); ++e) w[e] = v[e];
+  m1_mem<M>(w, r, u);
+#pragma unroll
+  for (int e = 0; e < (1 << M); ++e) v[e] = w[e];
 }
 
-template <int M, int A, typename V> __device__ __forceinline__ void d2_dispatch_b(V (&v)[1 << M], int b, const V* d) {
-  switch (b) {
-    GS_CASE1(M, 0, (d2_chk<M, A, 0>(v, d)))
-    GS_CASE1(M, 1, (d2_chk<M, A, 1>(v, d)))
-    GS_CASE1(M, 2, (d2_chk<M, A, 2>(v, d)))
-    GS_CASE1(M, 3, (d2_chk<M, A, 3>(v, d)))
-    GS_CASE1(M, 4, (d2_chk<M, A, 4>(v, d)))
+template <int M, typename V> __device__ __forceinline__ void m2_outofline(V (&v)[1 << M], int a, int b, const V* u) {
+  V w[1 << M];
+#pragma unroll
+  for (int e = 0; e < (1 << M); ++e) w[e] = v[e];
+  m2_mem<M>(w, a, b, u);
+#pragma unroll
+  for (int e = 0; e < (1 << M); ++e) v[e] = w[e];
+}
+
+template <typename T> struct V4;
+template <> struct V4<float> { using T = float4; };
+template <> struct V4<double> { using T = double4; };
+
+// factor p = {rs, t, sn, mode} on the elements e with (e & MASK) == WANT:
+// mode bit 0 -> real scale by rs, bit 1 -> shear rotation (t, sn); in place
+template <int M, int MASK, int WANT, typename V, typename P4>
+__device__ __forceinline__ void dparam_sel(V (&v)[1 << M], const P4 p) {
+  const int mode = (int)p.w;
+  if (mode & 1) {
+#pragma unroll
+    for (int e = 0; e < (1 << M); ++e)
+      if ((e & MASK) == WANT) v[e].x *= p.x, v[e].y *= p.x;
+  }
+  if (mode & 2) {
+#pragma unroll
+    for (int e = 0; e < (1 << M); ++e)
+      if ((e & MASK) == WANT) rot_inplace(v[e], p.y, p.z);
   }
 }
 
-template <int M, typename V> __device__ __forceinline__ void d2_dispatch(V (&v)[1 << M], int a, int b, const V* d) {
-  switch (a) {
-    GS_CASE1(M, 0, (d2_dispatch_b<M, 0>(v, b, d)))
-    GS_CASE1(M, 1, (d2_dispatch_b<M, 1>(v, b, d)))
-    GS_CASE1(M, 2, (d2_dispatch_b<M, 2>(v, b, d)))
-    GS_CASE1(M, 3, (d2_dispatch_b<M, 3>(v, b, d)))
-    GS_CASE1(M, 4, (d2_dispatch_b<M, 4>(v, b, d)))
-  }
-}
-
-template <int M, int A, typename V> __device__ __forceinline__ void m2_dispatch_b(V (&v)[1 << M], int b, const V* u) {
-  switch (b) {
-    GS_CASE1(M, 0, (m2_chk<M, A, 0>(v, u)))
-    GS_CASE1(M, 1, (m2_chk<M, A, 1>(v, u)))
-    GS_CASE1(M, 2, (m2_chk<M, A, 2>(v, u)))
-    GS_CASE1(M, 3, (m2_chk<M, A, 3>(v, u)))
-    GS_CASE1(M, 4, (m2_chk<M, A, 4>(v, u)))
-  }
-}
-
-template <int M, typename V> __device__ __forceinline__ void m2_dispatch(V (&v)[1 << M], int a, int b, const V* u) {
-  switch (a) {
-    GS_CASE1(M, 0, (m2_dispatch_b<M, 0>(v, b, u)))
-    GS_CASE1(M, 1, (m2_dispatch_b<M, 1>(v, b, u)))
-    GS_CASE1(M, 2, (m2_dispatch_b<M, 2>(v, b, u)))
-    GS_CASE1(M, 3, (m2_dispatch_b<M, 3>(v, b, u)))
-    GS_CASE1(M, 4, (m2_dispatch_b<M, 4>(v, b, u)))
-  }
-}
-
-__device__ __forceinline__ int bit_value(int where, int idx, int tb, long long base) {
+__device__ __forceinline__ int ubit(int where, int idx, int tb, long long base) {
   return where == B_THREAD ? ((tb >> idx) & 1) : (int)((base >> idx) & 1);
 }
 
+// one jump-table dispatch per primitive; every case updates v in place
 template <int M, typename V>
-__device__ __forceinline__ void apply_ops(V (&v)[1 << M], const Pass2Args& a, int ob, int oe, int tb,
-                                          long long base, int node_digit) {
+__device__ __forceinline__ void apply_prims(V (&v)[1 << M], const Pass2Args& a, int ob, int oe,
+                                            int tb, long long base, unsigned long long digits) {
+  using T = decltype(v[0].x);
+  using P4 = typename V4<T>::T;
+  const P4* params = reinterpret_cast<const P4*>(a.params);
   const V* coefs = reinterpret_cast<const V*>(a.coefs);
   for (int oi = ob; oi < oe; ++oi) {
-    const POp op = a.ops[oi];
-    int cofs = op.coef;
-    if (op.xtab >= 0) cofs = __ldg(a.xtable + op.xtab + (node_digit / op.xstride) % op.xradix);
-    const V* u = coefs + cofs;
-    switch (op.type) {
-      case P_W:
-        w_dispatch<M>(v, op.w, op.idx0);
-        break;
-      case P_M1:
-        m1_dispatch<M>(v, op.idx0, u);
-        break;
-      case P_D1:
-        if (op.where0 == B_REG) d1_dispatch<M>(v, op.idx0, u[0], u[1]);
-        else scale_all<M>(v, u[bit_value(op.where0, op.idx0, tb, base)]);
-        break;
-      case P_D2: {
-        const bool r0 = op.where0 == B_REG, r1 = op.where1 == B_REG;
-        if (r0 && r1) {
-          d2_dispatch<M>(v, op.idx0, op.idx1, u);
-        } else if (r0) {
-          const int b1 = bit_value(op.where1, op.idx1, tb, base);
-          d1_dispatch<M>(v, op.idx0, u[b1], u[2 + b1]);
-        } else if (r1) {
-          const int b0 = bit_value(op.where0, op.idx0, tb, base);
-          d1_dispatch<M>(v, op.idx1, u[2 * b0], u[2 * b0 + 1]);
-        } else {
-          const int b0 = bit_value(op.where0, op.idx0, tb, base);
-          const int b1 = bit_value(op.where1, op.idx1, tb, base);
-          scale_all<M>(v, u[2 * b0 + b1]);
-        }
-        break;
-      }
-      default:
-        m2_dispatch<M>(v, op.idx0, op.idx1, u);
-        break;
+    const PPrim op = a.prims[oi];
+    int poff = op.param;
+    if (op.flags & 1) poff = __ldg(a.pxtable + op.param + (int)((digits >> (4 * op.xk)) & 15)) + op.xsub;
+    int uv = 0;
+    if (op.code >= C_DHSEL && op.code <= C_DSEL) {
+      uv = ubit(op.ua_where, op.ua_idx, tb, base);
+      if (op.ub_where != 255) uv = 2 * uv + ubit(op.ub_where, op.ub_idx, tb, base);
+    }
+    switch (op.code) {
+      case 0: if constexpr (0 < M) w_reg<M, 0, 0>(v); break;
+      case 1: if constexpr (1 < M) w_reg<M, 1, 0>(v); break;
+      case 2: if constexpr (2 < M) w_reg<M, 2, 0>(v); break;
+      case 3: if constexpr (3 < M) w_reg<M, 3, 0>(v); break;
+      case 4: if constexpr (4 < M) w_reg<M, 4, 0>(v); break;
+      case 5: if constexpr (0 < M) w_reg<M, 0, 1>(v); break;
+      case 6: if constexpr (1 < M) w_reg<M, 1, 1>(v); break;
+      case 7: if constexpr (2 < M) w_reg<M, 2, 1>(v); break;
+      case 8: if constexpr (3 < M) w_reg<M, 3, 1>(v); break;
+      case 9: if constexpr (4 < M) w_reg<M, 4, 1>(v); break;
+      case 10: if constexpr (0 < M) w_reg<M, 0, 2>(v); break;
+      case 11: if constexpr (1 < M) w_reg<M, 1, 2>(v); break;
+      case 12: if constexpr (2 < M) w_reg<M, 2, 2>(v); break;
+      case 13: if constexpr (3 < M) w_reg<M, 3, 2>(v); break;
+      case 14: if constexpr (4 < M) w_reg<M, 4, 2>(v); break;
+      case 15: if constexpr (0 < M) dparam_sel<M, 1, 0>(v, params[poff]); break;
+      case 16: if constexpr (1 < M) dparam_sel<M, 2, 0>(v, params[poff]); break;
+      case 17: if constexpr (2 < M) dparam_sel<M, 4, 0>(v, params[poff]); break;
+      case 18: if constexpr (3 < M) dparam_sel<M, 8, 0>(v, params[poff]); break;
+      case 19: if constexpr (4 < M) dparam_sel<M, 16, 0>(v, params[poff]); break;
+      case 20: if constexpr (0 < M) dparam_sel<M, 1, 1>(v, params[poff]); break;
+      case 21: if constexpr (1 < M) dparam_sel<M, 2, 2>(v, params[poff]); break;
+      case 22: if constexpr (2 < M) dparam_sel<M, 4, 4>(v, params[poff]); break;
+      case 23: if constexpr (3 < M) dparam_sel<M, 8, 8>(v, params[poff]); break;
+      case 24: if constexpr (4 < M) dparam_sel<M, 16, 16>(v, params[poff]); break;
+      case 25: if constexpr (1 < M) dparam_sel<M, 3, 0>(v, params[poff]); break;
+      case 26: if constexpr (1 < M) dparam_sel<M, 3, 2>(v, params[poff]); break;
+      case 27: if constexpr (1 < M) dparam_sel<M, 3, 1>(v, params[poff]); break;
+      case 28: if constexpr (1 < M) dparam_sel<M, 3, 3>(v, params[poff]); break;
+      case 29: if constexpr (2 < M) dparam_sel<M, 5, 0>(v, params[poff]); break;
+      case 30: if constexpr (2 < M) dparam_sel<M, 5, 4>(v, params[poff]); break;
+      case 31: if constexpr (2 < M) dparam_sel<M, 5, 1>(v, params[poff]); break;
+      case 32: if constexpr (2 < M) dparam_sel<M, 5, 5>(v, params[poff]); break;
+      case 33: if constexpr (3 < M) dparam_sel<M, 9, 0>(v, params[poff]); break;
+      case 34: if constexpr (3 < M) dparam_sel<M, 9, 8>(v, params[poff]); break;
+      case 35: if constexpr (3 < M) dparam_sel<M, 9, 1>(v, params[poff]); break;
+      case 36: if constexpr (3 < M) dparam_sel<M, 9, 9>(v, params[poff]); break;
+      case 37: if constexpr (4 < M) dparam_sel<M, 17, 0>(v, params[poff]); break;
+      case 38: if constexpr (4 < M) dparam_sel<M, 17, 16>(v, params[poff]); break;
+      case 39: if constexpr (4 < M) dparam_sel<M, 17, 1>(v, params[poff]); break;
+      case 40: if constexpr (4 < M) dparam_sel<M, 17, 17>(v, params[poff]); break;
+      case 41: if constexpr (2 < M) dparam_sel<M, 6, 0>(v, params[poff]); break;
+      case 42: if constexpr (2 < M) dparam_sel<M, 6, 4>(v, params[poff]); break;
+      case 43: if constexpr (2 < M) dparam_sel<M, 6, 2>(v, params[poff]); break;
+      case 44: if constexpr (2 < M) dparam_sel<M, 6, 6>(v, params[poff]); break;
+      case 45: if constexpr (3 < M) dparam_sel<M, 10, 0>(v, params[poff]); break;
+      case 46: if constexpr (3 < M) dparam_sel<M, 10, 8>(v, params[poff]); break;
+      case 47: if constexpr (3 < M) dparam_sel<M, 10, 2>(v, params[poff]); break;
+      case 48: if constexpr (3 < M) dparam_sel<M, 10, 10>(v, params[poff]); break;
+      case 49: if constexpr (4 < M) dparam_sel<M, 18, 0>(v, params[poff]); break;
+      case 50: if constexpr (4 < M) dparam_sel<M, 18, 16>(v, params[poff]); break;
+      case 51: if constexpr (4 < M) dparam_sel<M, 18, 2>(v, params[poff]); break;
+      case 52: if constexpr (4 < M) dparam_sel<M, 18, 18>(v, params[poff]); break;
+      case 53: if constexpr (3 < M) dparam_sel<M, 12, 0>(v, params[poff]); break;
+      case 54: if constexpr (3 < M) dparam_sel<M, 12, 8>(v, params[poff]); break;
+      case 55: if constexpr (3 < M) dparam_sel<M, 12, 4>(v, params[poff]); break;
+      case 56: if constexpr (3 < M) dparam_sel<M, 12, 12>(v, params[poff]); break;
+      case 57: if constexpr (4 < M) dparam_sel<M, 20, 0>(v, params[poff]); break;
+      case 58: if constexpr (4 < M) dparam_sel<M, 20, 16>(v, params[poff]); break;
+      case 59: if constexpr (4 < M) dparam_sel<M, 20, 4>(v, params[poff]); break;
+      case 60: if constexpr (4 < M) dparam_sel<M, 20, 20>(v, params[poff]); break;
+      case 61: if constexpr (4 < M) dparam_sel<M, 24, 0>(v, params[poff]); break;
+      case 62: if constexpr (4 < M) dparam_sel<M, 24, 16>(v, params[poff]); break;
+      case 63: if constexpr (4 < M) dparam_sel<M, 24, 8>(v, params[poff]); break;
+      case 64: if constexpr (4 < M) dparam_sel<M, 24, 24>(v, params[poff]); break;
+      case 65: if constexpr (0 < M) dparam_sel<M, 1, 0>(v, params[poff + uv]); break;
+      case 66: if constexpr (1 < M) dparam_sel<M, 2, 0>(v, params[poff + uv]); break;
+      case 67: if constexpr (2 < M) dparam_sel<M, 4, 0>(v, params[poff + uv]); break;
+      case 68: if constexpr (3 < M) dparam_sel<M, 8, 0>(v, params[poff + uv]); break;
+      case 69: if constexpr (4 < M) dparam_sel<M, 16, 0>(v, params[poff + uv]); break;
+      case 70: if constexpr (0 < M) dparam_sel<M, 1, 1>(v, params[poff + uv]); break;
+      case 71: if constexpr (1 < M) dparam_sel<M, 2, 2>(v, params[poff + uv]); break;
+      case 72: if constexpr (2 < M) dparam_sel<M, 4, 4>(v, params[poff + uv]); break;
+      case 73: if constexpr (3 < M) dparam_sel<M, 8, 8>(v, params[poff + uv]); break;
+      case 74: if constexpr (4 < M) dparam_sel<M, 16, 16>(v, params[poff + uv]); break;
+      case 75: dparam_sel<M, 0, 0>(v, params[poff + uv]); break;
+      case 76: m1_outofline<M>(v, op.r0, coefs + poff); break;
+      default: m2_outofline<M>(v, op.r0, op.r1, coefs + poff); break;
     }
   }
 }
 
-// XOR swizzle of the low 4 (c64) / 3 (c128) address bits with higher bits:
-// bijective on [0, 2^K), spreads strided lane patterns across banks.
+// XOR swizzle of the low 4 (c64) / 3 (c128) address bits with the higher
+// nibbles: linear over GF(2) and bijective on [0, 2^K).  The host picks each
+// stage's lane bits so that their swizzled images are independent, which
+// makes every shared-memory exchange conflict-free.
 template <typename V> __device__ __forceinline__ int swz(int t) {
   constexpr int LB = sizeof(V) == 8 ? 4 : 3;
   constexpr int LM = (1 << LB) - 1;
-  return t ^ (((t >> LB) ^ (t >> (2 * LB)) ^ (t >> (3 * LB))) & LM);
+  return t ^ (((t >> LB) ^ (t >> (2 * LB)) ^ (t >> (3 * LB)) ^ (t >> (4 * LB))) & LM);
 }
 
-__device__ __forceinline__ int deposit(int x, unsigned mask, int K) {
-  int out = 0, n = 0;
-  for (int j = 0; j < K; ++j)
-    if ((mask >> j) & 1) out |= ((x >> n++) & 1) << j;
-  return out;
+// Gray-code walk over the 2^M register elements: element g(n) = n ^ (n >> 1)
+// differs from g(n-1) in bit ctz(n), so a linear address map costs one XOR.
+#define ctz_c(n) (((n) & 1) ? 0 : ((n) & 2) ? 1 : ((n) & 4) ? 2 : ((n) & 8) ? 3 : ((n) & 16) ? 4 : 5)
+
+
+template <int M>
+__device__ __forceinline__ int thread_tile_base(const PStage* st, int tid, int nthr_bits) {
+  int t = 0;
+  for (int j = 0; j < nthr_bits; ++j) t |= ((tid >> j) & 1) << st->tb[j];
+  return t;
 }
 
 template <typename R, int M>
-__global__ void __launch_bounds__(256) pass2_kernel(const Pass2Args a) {
+__global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass2Args a) {
   using V = typename Cx<R>::T;
   constexpr int E = 1 << M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* tile = reinterpret_cast<V*>(smem_raw);
   const int K = a.K;
-  int* hi_off = reinterpret_cast<int*>(tile + (1 << K));
+  const int nthr_bits = K - M;
   const int tid = threadIdx.x;
-  const int nt = blockDim.x;
-  const unsigned full = (1u << K) - 1;
 
   const long long group = (long long)(blockIdx.x >> a.tiles_log);
   const int tile_id = blockIdx.x & ((1 << a.tiles_log) - 1);
   long long base = 0;
   for (int j = 0; j < a.tiles_log; ++j) base |= (long long)((tile_id >> j) & 1) << a.gbits[j];
-  for (int h = tid; h < a.n_hi; h += nt) {
-    int off = 0;
-    for (int j = a.c; j < a.kq; ++j) off |= ((h >> (j - a.c)) & 1) << a.lbits[j];
-    hi_off[h] = off;
-  }
-  __syncthreads();
-  const int kqmask = (1 << a.kq) - 1;
-  const int cmask = (1 << a.c) - 1;
+  const int kq = a.kq;
+  const int kqmask = (1 << kq) - 1;
+
+  // global offset of a tile index: linear in its bits (tile bit j -> state bit lbits[j])
+  auto goff = [&](int t) {
+    long long o = 0;
+    for (int j = 0; j < kq; ++j) o |= (long long)((t >> j) & 1) << a.lbits[j];
+    return o;
+  };
 
   V v[E];
-  PStage st = a.stages[0];
-  int rbv[M];
-  unsigned rmask = 0;
-#pragma unroll
-  for (int i = 0; i < M; ++i) rbv[i] = 1 << st.rb[i], rmask |= rbv[i];
-  int tb = deposit(tid, full & ~rmask, K);
-  const long long slot = (group << (K - a.kq)) | (tb >> a.kq);
+  const PStage* st = a.stages;
+  int tb = thread_tile_base<M>(st, tid, nthr_bits);
+  const long long slot = (group << (K - kq)) | (tb >> kq);
   const bool active = slot < a.n_states;
-  const int node_digit = (a.digit && active) ? a.digit[slot] : 0;
+  const unsigned long long node_digits = (a.digits && active) ? a.digits[slot] : 0ull;
 
-  // stage 0: HBM -> registers
-  if (a.init_zero) {
+  // stage 0: HBM -> registers (register bits are high tile bits: lanes contiguous)
+  {
+    long long gstep[M];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      int t = tb;
+    for (int i = 0; i < M; ++i) gstep[i] = 1LL << a.lbits[st->rb[i]];
+    long long o = base | goff(tb & kqmask);
+    if (a.init_zero) {
 #pragma unroll
-      for (int i = 0; i < M; ++i)
-        if ((e >> i) & 1) t |= rbv[i];
-      const int tl = t & kqmask;
-      const long long off = base | (tl & cmask) | hi_off[tl >> a.c];
-      v[e].x = (off == 0) ? R(1) : R(0);
-      v[e].y = R(0);
+      for (int n = 0; n < E; ++n) {
+        if (n) o ^= gstep[ctz_c(n)];
+        const int e = n ^ (n >> 1);
+        v[e].x = (o == 0) ? R(1) : R(0);
+        v[e].y = R(0);
+      }
+    } else if (active) {
+      const long long ss = a.parent ? (long long)a.parent[slot] : slot;
+      const V* s = reinterpret_cast<const V*>(a.src) + ss * a.state_elems;
+#pragma unroll
+      for (int n = 0; n < E; ++n) {
+        if (n) o ^= gstep[ctz_c(n)];
+        v[n ^ (n >> 1)] = s[o];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e].x = v[e].y = R(0);
     }
-  } else if (active) {
-    const long long ss = a.parent ? (long long)a.parent[slot] : slot;
-    const V* s = reinterpret_cast<const V*>(a.src) + ss * a.state_elems + base;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      int t = tb;
-#pragma unroll
-      for (int i = 0; i < M; ++i)
-        if ((e >> i) & 1) t |= rbv[i];
-      const int tl = t & kqmask;
-      v[e] = s[(tl & cmask) | hi_off[tl >> a.c]];
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e].x = v[e].y = R(0);
   }
-  apply_ops<M>(v, a, st.op_begin, st.op_end, tb, base, node_digit);
+  apply_prims<M>(v, a, st->op_begin, st->op_end, tb, base, node_digits);
 
   for (int s = 1; s < a.n_stages; ++s) {
     if (s > 1) __syncthreads();
+    {
+      int sstep[M];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      int t = tb;
+      for (int i = 0; i < M; ++i) sstep[i] = swz<V>(1 << st->rb[i]);
+      int addr = swz<V>(tb);
 #pragma unroll
-      for (int i = 0; i < M; ++i)
-        if ((e >> i) & 1) t |= rbv[i];
-      tile[swz<V>(t)] = v[e];
+      for (int n = 0; n < E; ++n) {
+        if (n) addr ^= sstep[ctz_c(n)];
+        tile[addr] = v[n ^ (n >> 1)];
+      }
     }
     __syncthreads();
-    st = a.stages[s];
-    rmask = 0;
+    st = a.stages + s;
+    tb = thread_tile_base<M>(st, tid, nthr_bits);
+    {
+      int sstep[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) rbv[i] = 1 << st.rb[i], rmask |= rbv[i];
-    tb = deposit(tid, full & ~rmask, K);
+      for (int i = 0; i < M; ++i) sstep[i] = swz<V>(1 << st->rb[i]);
+      int addr = swz<V>(tb);
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      int t = tb;
-#pragma unroll
-      for (int i = 0; i < M; ++i)
-        if ((e >> i) & 1) t |= rbv[i];
-      v[e] = tile[swz<V>(t)];
+      for (int n = 0; n < E; ++n) {
+        if (n) addr ^= sstep[ctz_c(n)];
+        v[n ^ (n >> 1)] = tile[addr];
+      }
     }
-    apply_ops<M>(v, a, st.op_begin, st.op_end, tb, base, node_digit);
+    apply_prims<M>(v, a, st->op_begin, st->op_end, tb, base, node_digits);
   }
 
   // last stage: registers -> HBM
   if (!active) return;
-  V* d = reinterpret_cast<V*>(a.dst) + slot * a.state_elems + base;
+  V* d = reinterpret_cast<V*>(a.dst) + slot * a.state_elems;
   const R sc = (R)a.store_scale;
   const bool do_scale = a.store_scale != 1.0;
+  long long gstep[M];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    int t = tb;
+  for (int i = 0; i < M; ++i) gstep[i] = 1LL << a.lbits[st->rb[i]];
+  long long o = base | goff(tb & kqmask);
 #pragma unroll
-    for (int i = 0; i < M; ++i)
-      if ((e >> i) & 1) t |= rbv[i];
-    const int tl = t & kqmask;
-    V x = v[e];
+  for (int n = 0; n < E; ++n) {
+    if (n) o ^= gstep[ctz_c(n)];
+    V x = v[n ^ (n >> 1)];
     if (do_scale) x.x *= sc, x.y *= sc;
-    d[(tl & cmask) | hi_off[tl >> a.c]] = x;
+    d[o] = x;
   }
 }
 

@@ -5,42 +5,52 @@
 
 namespace gs {
 
-enum PassOpType : int8_t {
-  P_W = 0,   // W-form on register bit idx0; w = 0 H, 1 X^1/2, 2 Y^1/2
-  P_M1 = 1,  // dense 2x2 on register bit idx0
-  P_D1 = 2,  // diag(d0, d1) on bit 0
-  P_D2 = 3,  // diag(d00, d01, d10, d11) on bits (0, 1) = (qa, qb)
-  P_M2 = 4,  // dense 4x4 on register bits (idx0 = qa, idx1 = qb)
-};
-
 // bit location of a diagonal op's qubit in the current stage
 enum BitWhere : int8_t { B_REG = 0, B_THREAD = 1, B_TILE = 2 };
 
-struct POp {
-  int8_t type, w;
-  int8_t where0, where1;
-  int8_t idx0, idx1;  // register bit, tile bit (B_THREAD) or state bit (B_TILE)
-  int16_t pad;
-  int32_t coef;
-  int32_t xtab;  // >= 0: cross op, coef = xtable[xtab + digit]
-  int32_t xstride;
-  int32_t xradix;
-};
 
 struct PStage {
-  int8_t rb[8];  // register bit i -> tile bit
+  int8_t rb[8];   // register bit i -> tile bit
+  int8_t tb[16];  // thread-index bit j -> tile bit (lanes = j < 5)
   int32_t op_begin, op_end;
+};
+
+// Flattened primitive of the v2 pass: one jump-table case per (kind, register
+// bit(s)); diagonal factors are pre-split by the host into real scale `rs` and
+// shear-rotation parameters (t = tan(theta/2), sn = sin(theta)).
+enum PrimCode : uint8_t {
+  C_W = 0,        // + w*5 + b      W-form (H, X^1/2, Y^1/2) on register bit b
+  C_DH = 15,      // + h*5 + b      diag factor on the half where bit b == h
+  C_DQ = 25,      // + pair*4 + q   diag factor on quadrant q of register pair
+  C_DHSEL = 65,   // + h*5 + b      like C_DH, factor selected by uniform bit ua
+  C_DSEL = 75,    //                factor on every element, selected by ua (, ub)
+  C_M1 = 76,      //                dense 2x2 on register bit r0 (out of line)
+  C_M2 = 77,      //                dense 4x4 on register bits (r0 = qa, r1 = qb)
+  C_NCODES = 78,
+};
+
+struct PPrim {
+  uint8_t code;
+  uint8_t ua_where, ua_idx;  // uniform bit A: where (B_THREAD / B_TILE), index
+  uint8_t ub_where, ub_idx;  // uniform bit B (C_DSEL on two bits), where = 255: none
+  uint8_t r0, r1;            // register bits for C_M1 / C_M2
+  uint8_t xk;                // cross op: nibble of the node's packed digits
+  int32_t param;             // param offset, or xtable base for cross ops
+  int16_t xsub;              // cross op: added to the xtable entry
+  int16_t flags;             // bit 0: cross op
 };
 
 struct Pass2Args {
   const void* src;
   void* dst;
   const int32_t* parent;
-  const int32_t* digit;
-  const POp* ops;
   const PStage* stages;
   const void* coefs;
   const int32_t* xtable;
+  const PPrim* prims;
+  const void* params;        // float4 / double4 {rs, t, sn, mode}
+  const int32_t* pxtable;    // cross op: digit -> param offset
+  const unsigned long long* digits;  // packed 4-bit digits per child state
   long long state_elems;
   long long n_states;
   double store_scale;  // power of two, applied on store

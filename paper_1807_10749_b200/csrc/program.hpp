@@ -55,6 +55,7 @@ struct PassPlan {
   int64_t dev_op_offset = 0;    // into the device op array (v1 kernel)
   std::vector<StagePlan> stages;
   int M = 0;                    // register bits per stage
+  int K = 0;                    // tile bits incl. slot bits (v2 kernel)
   int64_t dev_stage_offset = 0; // into the device stage array
   double store_scale = 1.0;     // power of two applied on store
 };
