@@ -66,69 +66,88 @@ template <int M, int B, int W, typename V> __device__ __forceinline__ void w_reg
   }
 }
 
-// coefficient load that the compiler may not hoist out of the unrolled group
-// loop (keeps a 4x4's 16 complex entries out of the register file)
-__device__ __forceinline__ float2 ld_coef(const float2* p) {
-  float2 r;
-  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ double2 ld_coef(const double2* p) {
-  double2 r;
-  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
-  return r;
+// XOR swizzle of the low 4 (c64) / 3 (c128) address bits with the higher
+// nibbles: linear over GF(2) and bijective on [0, 2^K).  The host picks each
+// stage's lane bits so that their swizzled images are independent, which
+// makes every shared-memory exchange conflict-free.
+template <typename V> __device__ __forceinline__ int swz(int t) {
+  constexpr int LB = sizeof(V) == 8 ? 4 : 3;
+  constexpr int LM = (1 << LB) - 1;
+  return t ^ (((t >> LB) ^ (t >> (2 * LB)) ^ (t >> (3 * LB)) ^ (t >> (4 * LB))) & LM);
 }
 
+// Gray-code walk over the 2^M register elements: element g(n) = n ^ (n >> 1)
+// differs from g(n-1) in bit ctz(n), so a linear address map costs one XOR.
+#define ctz_c(n) (((n) & 1) ? 0 : ((n) & 2) ? 1 : ((n) & 4) ? 2 : ((n) & 8) ? 3 : ((n) & 16) ? 4 : 5)
 
 
-// Dense 2x2 / 4x4 ops cannot be done in place; they run out of line on a
-// local copy of the registers so the hot in-place paths keep a fixed register
-// assignment (see the note above dkind).
-template <int M, typename V> __device__ __noinline__ void m1_mem(V* w, int r, const V* u) {
-  const V u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
-  for (int e = 0; e < (1 << M); ++e) {
-    if ((e >> r) & 1) continue;
-    const V x0 = w[e], x1 = w[e | (1 << r)];
-    w[e] = cmad2(u00, x0, u01, x1);
-    w[e | (1 << r)] = cmad2(u10, x0, u11, x1);
-  }
-}
-
-template <int M, typename V> __device__ __noinline__ void m2_mem(V* w, int a, int b, const V* u) {
-  for (int e = 0; e < (1 << M); ++e) {
-    if (((e >> a) & 1) || ((e >> b) & 1)) continue;
-    V x[4];
-    for (int s = 0; s < 4; ++s) x[s] = w[e | ((s >> 1) << a) | ((s & 1) << b)];
-    for (int r = 0; r < 4; ++r) {
-      V y;
-      y.x = 0;
-      y.y = 0;
-      for (int s = 0; s < 4; ++s) {
-        const V c = u[4 * r + s];
-        y.x += c.x * x[s].x - c.y * x[s].y;
-        y.y += c.x * x[s].y + c.y * x[s].x;
-      }
-      w[e | ((r >> 1) << a) | ((r & 1) << b)] = y;
+// Dense 2x2 / 4x4 ops (cross-gate Schmidt terms, intra-block iSWAP / fSim)
+// cannot update registers in place.  The thread parks its 2^M amplitudes in
+// its own slots of the shared tile (slots no other thread touches in this
+// stage), applies the op there with runtime bit indices, and reloads: no
+// call, no local memory, and the hot in-place paths keep their registers.
+template <int M, typename V>
+__device__ __forceinline__ void dense_op(V (&v)[1 << M], V* tile, const PStage* st, int tb, bool two,
+                                         int r0, int r1, const V* u) {
+  constexpr int E = 1 << M;
+  int sstep[M];
+#pragma unroll
+  for (int i = 0; i < M; ++i) sstep[i] = swz<V>(1 << st->rb[i]);
+  const int base = swz<V>(tb);
+  {
+    int addr = base;
+#pragma unroll
+    for (int n = 0; n < E; ++n) {
+      if (n) addr ^= sstep[ctz_c(n)];
+      tile[addr] = v[n ^ (n >> 1)];
     }
   }
-}
-
-template <int M, typename V> __device__ __forceinline__ void m1_outofline(V (&v)[1 << M], int r, const V* u) {
-  V w[1 << M];
+  auto slot = [&](int e) {
+    int a = base;
 #pragma unroll
-  for (int e = 0; e < (1 << M); ++e) w[e] = v[e];
-  m1_mem<M>(w, r, u);
+    for (int i = 0; i < M; ++i)
+      if ((e >> i) & 1) a ^= sstep[i];
+    return a;
+  };
+  if (!two) {
+    const V u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+    for (int e = 0; e < E; ++e) {
+      if ((e >> r0) & 1) continue;
+      const int a0 = slot(e), a1 = slot(e | (1 << r0));
+      const V x0 = tile[a0], x1 = tile[a1];
+      tile[a0] = cmad2(u00, x0, u01, x1);
+      tile[a1] = cmad2(u10, x0, u11, x1);
+    }
+  } else {
+    for (int e = 0; e < E; ++e) {
+      if (((e >> r0) & 1) || ((e >> r1) & 1)) continue;
+      int ad[4];
+      V x[4];
 #pragma unroll
-  for (int e = 0; e < (1 << M); ++e) v[e] = w[e];
-}
-
-template <int M, typename V> __device__ __forceinline__ void m2_outofline(V (&v)[1 << M], int a, int b, const V* u) {
-  V w[1 << M];
+      for (int q = 0; q < 4; ++q) ad[q] = slot(e | ((q >> 1) << r0) | ((q & 1) << r1)), x[q] = tile[ad[q]];
 #pragma unroll
-  for (int e = 0; e < (1 << M); ++e) w[e] = v[e];
-  m2_mem<M>(w, a, b, u);
+      for (int r = 0; r < 4; ++r) {
+        V y;
+        y.x = 0;
+        y.y = 0;
 #pragma unroll
-  for (int e = 0; e < (1 << M); ++e) v[e] = w[e];
+        for (int q = 0; q < 4; ++q) {
+          const V c = u[4 * r + q];
+          y.x += c.x * x[q].x - c.y * x[q].y;
+          y.y += c.x * x[q].y + c.y * x[q].x;
+        }
+        tile[ad[r]] = y;
+      }
+    }
+  }
+  {
+    int addr = base;
+#pragma unroll
+    for (int n = 0; n < E; ++n) {
+      if (n) addr ^= sstep[ctz_c(n)];
+      v[n ^ (n >> 1)] = tile[addr];
+    }
+  }
 }
 
 template <typename T> struct V4;
@@ -159,15 +178,29 @@ __device__ __forceinline__ int ubit(int where, int idx, int tb, long long base) 
 // one jump-table dispatch per primitive; every case updates v in place
 template <int M, typename V>
 __device__ __forceinline__ void apply_prims(V (&v)[1 << M], const Pass2Args& a, int ob, int oe,
-                                            int tb, long long base, unsigned long long digits) {
+                                            int tb, long long base, unsigned long long digits,
+                                            V* tile, const PStage* st) {
   using T = decltype(v[0].x);
   using P4 = typename V4<T>::T;
   const P4* params = reinterpret_cast<const P4*>(a.params);
   const V* coefs = reinterpret_cast<const V*>(a.coefs);
+  const uint4* prims = reinterpret_cast<const uint4*>(a.prims);
   for (int oi = ob; oi < oe; ++oi) {
-    const PPrim op = a.prims[oi];
-    int poff = op.param;
-    if (op.flags & 1) poff = __ldg(a.pxtable + op.param + (int)((digits >> (4 * op.xk)) & 15)) + op.xsub;
+    const uint4 raw = __ldg(prims + oi);  // PPrim, one 16-byte load
+    struct {
+      int code, ua_where, ua_idx, ub_where, ub_idx, r0, r1;
+    } op;
+    op.code = raw.x & 0xff;
+    op.ua_where = (raw.x >> 8) & 0xff;
+    op.ua_idx = (raw.x >> 16) & 0xff;
+    op.ub_where = raw.x >> 24;
+    op.ub_idx = raw.y & 0xff;
+    op.r0 = (raw.y >> 8) & 0xff;
+    op.r1 = (raw.y >> 16) & 0xff;
+    const int xk = raw.y >> 24;
+    int poff = (int)raw.z;
+    if (raw.w & 0x10000u)  // cross op
+      poff = __ldg(a.pxtable + poff + (int)((digits >> (4 * xk)) & 15)) + (int)(short)(raw.w & 0xffff);
     int uv = 0;
     if (op.code >= C_DHSEL && op.code <= C_DSEL) {
       uv = ubit(op.ua_where, op.ua_idx, tb, base);
@@ -250,26 +283,11 @@ __device__ __forceinline__ void apply_prims(V (&v)[1 << M], const Pass2Args& a, 
       case 73: if constexpr (3 < M) dparam_sel<M, 8, 8>(v, params[poff + uv]); break;
       case 74: if constexpr (4 < M) dparam_sel<M, 16, 16>(v, params[poff + uv]); break;
       case 75: dparam_sel<M, 0, 0>(v, params[poff + uv]); break;
-      case 76: m1_outofline<M>(v, op.r0, coefs + poff); break;
-      default: m2_outofline<M>(v, op.r0, op.r1, coefs + poff); break;
+      case 76: dense_op<M>(v, tile, st, tb, false, op.r0, 0, coefs + poff); break;
+      default: dense_op<M>(v, tile, st, tb, true, op.r0, op.r1, coefs + poff); break;
     }
   }
 }
-
-// XOR swizzle of the low 4 (c64) / 3 (c128) address bits with the higher
-// nibbles: linear over GF(2) and bijective on [0, 2^K).  The host picks each
-// stage's lane bits so that their swizzled images are independent, which
-// makes every shared-memory exchange conflict-free.
-template <typename V> __device__ __forceinline__ int swz(int t) {
-  constexpr int LB = sizeof(V) == 8 ? 4 : 3;
-  constexpr int LM = (1 << LB) - 1;
-  return t ^ (((t >> LB) ^ (t >> (2 * LB)) ^ (t >> (3 * LB)) ^ (t >> (4 * LB))) & LM);
-}
-
-// Gray-code walk over the 2^M register elements: element g(n) = n ^ (n >> 1)
-// differs from g(n-1) in bit ctz(n), so a linear address map costs one XOR.
-#define ctz_c(n) (((n) & 1) ? 0 : ((n) & 2) ? 1 : ((n) & 4) ? 2 : ((n) & 8) ? 3 : ((n) & 16) ? 4 : 5)
-
 
 template <int M>
 __device__ __forceinline__ int thread_tile_base(const PStage* st, int tid, int nthr_bits) {
@@ -336,7 +354,7 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
       for (int e = 0; e < E; ++e) v[e].x = v[e].y = R(0);
     }
   }
-  apply_prims<M>(v, a, st->op_begin, st->op_end, tb, base, node_digits);
+  apply_prims<M>(v, a, st->op_begin, st->op_end, tb, base, node_digits, tile, st);
 
   for (int s = 1; s < a.n_stages; ++s) {
     if (s > 1) __syncthreads();
@@ -365,7 +383,7 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
         v[n ^ (n >> 1)] = tile[addr];
       }
     }
-    apply_prims<M>(v, a, st->op_begin, st->op_end, tb, base, node_digits);
+    apply_prims<M>(v, a, st->op_begin, st->op_end, tb, base, node_digits, tile, st);
   }
 
   // last stage: registers -> HBM

@@ -39,6 +39,7 @@ struct PPrim {
   int16_t xsub;              // cross op: added to the xtable entry
   int16_t flags;             // bit 0: cross op
 };
+static_assert(sizeof(PPrim) == 16, "PPrim is loaded as one uint4");
 
 struct Pass2Args {
   const void* src;
