@@ -116,6 +116,11 @@ int gs_load_program(gs_ctx* ctx, int32_t n_qubits_a, int32_t n_qubits_b, int32_t
                     const int64_t* term_coef_a, const int32_t* term_kind_b,
                     const int64_t* term_coef_b, int64_t n_coef, const double* coef_re_im);
 
+/* JSON description of the loaded program's schedule (levels, passes per block,
+ * register stages and primitives per stage) for diagnostics.  Writes at most
+ * cap bytes (NUL-terminated) to buf; *needed receives the full size. */
+int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed);
+
 /* Requested amplitudes as block-local indices (split_requests, pathsum.py:122-140).
  * Host arrays; validated against the loaded program's block sizes and uploaded. */
 int gs_set_requests(gs_ctx* ctx, int64_t n_req, const int64_t* idx_a, const int64_t* idx_b);

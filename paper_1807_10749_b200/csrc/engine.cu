@@ -134,6 +134,7 @@ struct Ctx {
   std::vector<PStage> host_pstages;
   double kfinal[2][2] = {{1, 0}, {1, 0}};  // per block: true = stored * K
   int kernel_version = 2;
+  int hoist = 1;  // move digit-independent ops above branch points
   int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
   // requests
   int64_t n_req = -1;
@@ -190,6 +191,31 @@ static void classify_w(HostOp& op, const double* u) {
   else if (eq(1, si, -sr) && eq(2, si, -sr) && eq(3, sr, si)) op.w = 1;           // X: -i*s
   else if (eq(1, -sr, -si) && eq(2, sr, si) && eq(3, sr, si)) op.w = 2;           // Y
   if (op.w >= 0) op.s_re = sr, op.s_im = si;
+}
+
+// Move every segment op that commutes with its level's cross terms (and with
+// the ops it would pass) above the branch point: it is then applied once per
+// parent node instead of once per child.  Processed from the deepest level up,
+// so an op keeps rising while it commutes.  Exact (commutation), so results
+// match the reference op order up to rounding.
+static void hoist_ops(Program& p) {
+  for (int l = (int)p.levels.size() - 1; l >= 1; --l) {
+    Level& L = p.levels[l];
+    Level& P = p.levels[l - 1];
+    for (int side = 0; side < 2; ++side) {
+      std::vector<HostOp> stay, up;
+      for (const HostOp& op : L.ops[side]) {
+        bool ok = op.cross < 0;
+        if (ok)
+          for (const HostOp& b : stay)
+            if (ops_conflict(op, b)) { ok = false; break; }
+        (ok ? up : stay).push_back(op);
+      }
+      if (up.empty()) continue;
+      P.ops[side].insert(P.ops[side].end(), up.begin(), up.end());
+      L.ops[side] = std::move(stay);
+    }
+  }
 }
 
 static void build_program(Ctx& c, int qa, int qb, int n_ops, const int32_t* kind,
@@ -303,6 +329,7 @@ static void build_program(Ctx& c, int qa, int qb, int n_ops, const int32_t* kind
     p.levels[l].ops[side].push_back(op);
   }
   if (seen_cross != n_cross) throw GsError(GS_ERR_ARG, "cross op count mismatch");
+  if (c.hoist) hoist_ops(p);
   c.prog = std::move(p);
 }
 
@@ -1115,6 +1142,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "low_bits out of range");
       c.low_bits = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "hoist") {
+      c.hoist = value ? 1 : 0;
+      if (c.have_prog) throw GsError(GS_ERR_STATE, "set hoist before gs_load_program");
     } else if (k == "reg_bits") {
       if (value != 4 && value != 5) throw GsError(GS_ERR_ARG, "reg_bits must be 4 or 5");
       c.reg_bits = (int)value;
@@ -1154,6 +1184,45 @@ int gs_load_program(gs_ctx* ctx, int32_t qa, int32_t qb, int32_t n_ops, const in
     gs::upload_program(c);
     c.have_prog = true;
     c.n_req = -1;
+  });
+}
+
+int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
+  if (!ctx) return GS_ERR_ARG;
+  GS_GUARD(ctx, {
+    Ctx& c = ctx->c;
+    if (!c.have_prog) throw GsError(GS_ERR_STATE, "no program loaded");
+    std::string js = "{\"q\": [" + std::to_string(c.prog.q[0]) + ", " + std::to_string(c.prog.q[1]) +
+                     "], \"levels\": [";
+    for (size_t l = 0; l < c.prog.levels.size(); ++l) {
+      const gs::Level& L = c.prog.levels[l];
+      js += (l ? ", " : "") + std::string("{\"k_lo\": ") + std::to_string(L.k_lo) +
+            ", \"k_hi\": " + std::to_string(L.k_hi) + ", \"blocks\": [";
+      for (int side = 0; side < 2; ++side) {
+        js += (side ? ", " : "") + std::string("{\"ops\": ") + std::to_string(L.ops[side].size()) +
+              ", \"passes\": [";
+        for (size_t pi = 0; pi < L.passes[side].size(); ++pi) {
+          const gs::PassPlan& pp = L.passes[side][pi];
+          js += (pi ? ", " : "") + std::string("{\"ops\": ") + std::to_string(pp.ops.size()) +
+                ", \"k\": " + std::to_string(pp.k) + ", \"K\": " + std::to_string(pp.K) +
+                ", \"M\": " + std::to_string(pp.M) + ", \"stages\": [";
+          for (size_t si = 0; si < pp.stages.size(); ++si) {
+            const gs::PStage& ps = c.host_pstages[pp.dev_stage_offset + si];
+            js += (si ? ", " : "") + std::to_string(ps.op_end - ps.op_begin);
+          }
+          js += "], \"store_scale\": " + std::to_string(pp.store_scale) + "}";
+        }
+        js += "]}";
+      }
+      js += "]}";
+    }
+    js += "]}";
+    if (needed) *needed = (int64_t)js.size() + 1;
+    if (buf && cap > 0) {
+      const size_t n = std::min<size_t>(js.size(), (size_t)cap - 1);
+      std::memcpy(buf, js.data(), n);
+      buf[n] = 0;
+    }
   });
 }
 

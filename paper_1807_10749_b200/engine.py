@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = (
     "gs_load_program",
     "gs_set_requests",
     "gs_run",
+    "gs_describe",
 )
 
 
@@ -91,6 +92,7 @@ def _load():
         ctypes.c_int64, _F64P,
     ]
     lib.gs_set_requests.argtypes = [_P, ctypes.c_int64, _I64P, _I64P]
+    lib.gs_describe.argtypes = [_P, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
     lib.gs_run.argtypes = [
         _P, ctypes.c_int32, ctypes.c_int64, _I64P, ctypes.c_int64, ctypes.c_int64,
         _F64P, _P, ctypes.c_int32, ctypes.POINTER(GsStats),
@@ -215,6 +217,15 @@ class Engine:
         self._program = prog
         self._requests = None
         self.n_req = -1
+
+    def describe(self) -> dict:
+        import json
+
+        need = ctypes.c_int64(0)
+        self._check(LIB.gs_describe(self._h, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(int(need.value))
+        self._check(LIB.gs_describe(self._h, buf, need.value, ctypes.byref(need)))
+        return json.loads(buf.value.decode())
 
     def set_requests(self, idx_a: np.ndarray, idx_b: np.ndarray, key=None):
         if key is not None and self._requests is not None and self._requests == key:
