@@ -135,6 +135,8 @@ struct Ctx {
   double kfinal[2][2] = {{1, 0}, {1, 0}};  // per block: true = stored * K
   int kernel_version = 2;
   int hoist = 1;  // move digit-independent ops above branch points
+  int smem_gather = 1;
+  DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
   int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
   // requests
   int64_t n_req = -1;
@@ -155,6 +157,7 @@ struct Ctx {
   std::vector<int64_t> cap;        // nodes per level buffer
   std::vector<int> lvl_end;        // digit end e_l per level
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<std::vector<Node>> kids;  // per-level child scratch for the DFS
 
   size_t esize() const { return precision == GS_C64 ? 8 : 16; }
   int kmax() const {
@@ -494,6 +497,8 @@ static void emit_prims(Ctx& c, int side, const Level& L, const HostOp& op, const
   }
 }
 
+static uint64_t pack_level_digits(const Program& p, int l, int64_t v);
+
 static void schedule_program(Ctx& c) {
   Program& p = c.prog;
   c.host_devops.clear();
@@ -614,6 +619,17 @@ static void schedule_program(Ctx& c) {
     c.kfinal[side][0] = kre;
     c.kfinal[side][1] = kim;
   }
+  // packed-digit lookup per level (fan-outs up to 2^16)
+  for (size_t l = 1; l < p.levels.size(); ++l) {
+    Level& L = p.levels[l];
+    L.packed.clear();
+    int64_t F = 1;
+    for (int k = L.k_lo; k < L.k_hi; ++k) F *= p.radix[k];
+    if (F > 65536) continue;
+    std::vector<uint64_t> tab(F);
+    for (int64_t v = 0; v < F; ++v) tab[v] = pack_level_digits(p, (int)l, v);
+    L.packed = std::move(tab);
+  }
   // level digit products must fit int32 node digits
   for (size_t l = 1; l < p.levels.size(); ++l) {
     int64_t f = 1;
@@ -662,6 +678,7 @@ static int64_t level_fanout(const Program& p, int l) {
 // mixed-radix level digit value -> packed nibbles (gate k_lo + j at bits 4j)
 static uint64_t pack_level_digits(const Program& p, int l, int64_t v) {
   const Level& L = p.levels[l];
+  if (v < (int64_t)L.packed.size()) return L.packed[v];
   uint64_t out = 0;
   for (int k = L.k_hi - 1; k >= L.k_lo; --k) {
     out |= (uint64_t)(v % p.radix[k]) << (4 * (k - L.k_lo));
@@ -873,8 +890,7 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
     c.st.pass_bytes_min += 2.0 * (double)n * (double)(1LL << c.prog.q[side]) * (double)c.esize();
 }
 
-template <typename R> static void gather(Ctx& c, int l, const std::vector<Node>& nodes) {
-  const int64_t n = (int64_t)nodes.size();
+template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64_t n) {
   // leaf multiplicity: duplicate prefixes / branch ranges collapsed into one node
   int64_t w_total = 0;
   for (int64_t j = 0; j < n; ++j) w_total += (nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0);
@@ -902,12 +918,37 @@ template <typename R> static void gather(Ctx& c, int l, const std::vector<Node>&
   groups = (n + per - 1) / per;
   c.d_partial.ensure((size_t)groups * nreq * sizeof(double2));
   const int qa = c.prog.q[0], qb = c.prog.q[1];
+  const size_t pair_bytes = ((size_t)1 << qa) * c.esize() + ((size_t)1 << qb) * c.esize();
+  if (c.smem_gather && 2 * pair_bytes <= 200 * 1024 && qa + qb <= 31 && qa >= 2 && qb >= 2) {
+    // shared-memory gather: whole leaf pairs staged per CTA, requests in registers
+    constexpr int RPT = 20, NT = 512;
+    const int64_t req_per_cta = (int64_t)RPT * NT;
+    const int64_t xb = (nreq + req_per_cta - 1) / req_per_cta;
+    int64_t g = std::max<int64_t>(1, (148 + xb - 1) / xb);
+    g = std::min<int64_t>(g, n);
+    g = std::min<int64_t>(g, std::max<int64_t>(1, (256LL << 20) / (16 * nreq)));
+    const int64_t per2 = (n + g - 1) / g;
+    g = (n + per2 - 1) / per2;
+    c.d_partial.ensure((size_t)g * nreq * sizeof(double2));
+    static bool configured[2] = {false, false};
+    if (!configured[sizeof(R) == 8]) {
+      CK(cudaFuncSetAttribute(gather_smem_kernel<R, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+      configured[sizeof(R) == 8] = true;
+    }
+    gather_smem_kernel<R, RPT><<<dim3((unsigned)xb, (unsigned)g), NT, 2 * pair_bytes, c.stream>>>(
+        c.lvl_a[l].p, c.lvl_b[l].p, qa, qb, (int)n, (int)per2,
+        reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const uint32_t*>(c.d_packed.p),
+        nreq, (int)req_per_cta, reinterpret_cast<double2*>(c.d_partial.p));
+    launch_check("gather_smem_kernel", xb * g, NT, 2 * pair_bytes);
+    groups = g;
+  } else {
   dim3 grid((unsigned)xblocks, (unsigned)groups);
   gather_kernel<R><<<grid, threads, 0, c.stream>>>(
       c.lvl_a[l].p, c.lvl_b[l].p, 1LL << qa, 1LL << qb, (int)n, (int)per,
       reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const int32_t*>(c.d_ia.p),
       reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
   launch_check("gather_kernel", xblocks * groups, threads, 0);
+  }
   double2 kf = make_double2(1.0, 0.0);
   if (c.kernel_version == 2) {  // deferred W-form scalars of both blocks
     const double ar = c.kfinal[0][0], ai = c.kfinal[0][1], br = c.kfinal[1][0], bi = c.kfinal[1][1];
@@ -922,19 +963,20 @@ template <typename R> static void gather(Ctx& c, int l, const std::vector<Node>&
   c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
 }
 
-template <typename R> static void descend(Ctx& c, int l, const std::vector<Node>& nodes) {
+template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int64_t n_nodes) {
   const int D = (int)c.prog.levels.size() - 1;
   if (l == D) {
-    gather<R>(c, l, nodes);
+    gather<R>(c, l, nodes, n_nodes);
     return;
   }
-  std::vector<Node> kids;
-  enumerate_children(c, l, nodes.data(), (int64_t)nodes.size(), kids);
+  std::vector<Node>& kids = c.kids[l + 1];  // per-level scratch, reused across chunks
+  kids.clear();
+  enumerate_children(c, l, nodes, n_nodes, kids);
   const int64_t cap = c.cap[l + 1];
-  const size_t ea = (size_t)(1LL << c.prog.q[0]), eb = (size_t)(1LL << c.prog.q[1]);
+  auto at = [](std::vector<DevBuf>& v, int i) -> void* { return i < (int)v.size() ? v[i].p : nullptr; };
   for (int64_t s = 0; s < (int64_t)kids.size(); s += cap) {
     const int64_t n = std::min<int64_t>(cap, (int64_t)kids.size() - s);
-    std::vector<Node> chunk(kids.begin() + s, kids.begin() + s + n);
+    const Node* chunk = kids.data() + s;
     if (!c.host_only) {
       PinnedBuf& stg = c.lvl_stage[l + 1];
       cudaEventSynchronize(c.lvl_event[l + 1]);
@@ -946,13 +988,10 @@ template <typename R> static void descend(Ctx& c, int l, const std::vector<Node>
       c.st.h2d_bytes += 12.0 * n;
       CK(cudaEventRecord(c.lvl_event[l + 1], c.stream));
     }
-    auto at = [](std::vector<DevBuf>& v, int i) -> void* { return i < (int)v.size() ? v[i].p : nullptr; };
     run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
                         at(c.lvl_b, l + 1), reinterpret_cast<const int32_t*>(at(c.lvl_parent, l + 1)),
                         reinterpret_cast<const uint64_t*>(at(c.lvl_digit, l + 1)), false);
-    (void)ea;
-    (void)eb;
-    descend<R>(c, l + 1, chunk);
+    descend<R>(c, l + 1, chunk, n);
   }
 }
 
@@ -1023,9 +1062,10 @@ static void run_tree(Ctx& c) {
   // root: |0...0> through the root segment
   run_level_passes<R>(c, 0, 1, nullptr, nullptr, c.lvl_a.empty() ? nullptr : c.lvl_a[0].p,
                       c.lvl_b.empty() ? nullptr : c.lvl_b[0].p, nullptr, nullptr, true);
-  std::vector<Node> root{{0, (int64_t)c.prefixes.size(), 0, 0, c.branch_lo, c.branch_hi, 0, 0}};
+  const Node root{0, (int64_t)c.prefixes.size(), 0, 0, c.branch_lo, c.branch_hi, 0, 0};
   if (c.prefixes.empty() || c.branch_hi <= c.branch_lo) return;
-  descend<R>(c, 0, root);
+  c.kids.resize(D + 1);
+  descend<R>(c, 0, &root, 1);
 }
 
 }  // namespace gs
@@ -1145,6 +1185,8 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "hoist") {
       c.hoist = value ? 1 : 0;
       if (c.have_prog) throw GsError(GS_ERR_STATE, "set hoist before gs_load_program");
+    } else if (k == "smem_gather") {
+      c.smem_gather = value ? 1 : 0;
     } else if (k == "reg_bits") {
       if (value != 4 && value != 5) throw GsError(GS_ERR_ARG, "reg_bits must be 4 or 5");
       c.reg_bits = (int)value;
@@ -1244,6 +1286,11 @@ int gs_set_requests(gs_ctx* ctx, int64_t n_req, const int64_t* ia, const int64_t
       CK(cudaSetDevice(c.device));
       gs::upload(c, c.d_ia, a);
       gs::upload(c, c.d_ib, b);
+      if (c.prog.q[0] + c.prog.q[1] <= 31) {
+        std::vector<uint32_t> pk(n_req);
+        for (int64_t i = 0; i < n_req; ++i) pk[i] = (uint32_t)a[i] | ((uint32_t)b[i] << c.prog.q[0]);
+        gs::upload(c, c.d_packed, pk);
+      }
       c.d_acc.ensure(std::max<size_t>(n_req * sizeof(double2), 16));
     }
     c.n_req = n_req;

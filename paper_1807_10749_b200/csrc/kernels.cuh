@@ -223,3 +223,84 @@ reduce_kernel(const double2* partial, int groups, long long n_req, double2 k, do
 }
 
 }  // namespace gs
+
+namespace gs {
+
+// ---------------------------------------------------------------------------
+// Shared-memory gather for small half-states (pair <= ~96 KB): a CTA streams a
+// group of leaves through a cp.async double buffer (each leaf pair read from
+// HBM exactly once, coalesced) while every thread keeps the fp64 accumulators
+// of its RPT requests in registers.  Requests are packed ia | ib << qa.
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <typename R, int RPT>
+__global__ void __launch_bounds__(512, 1)
+gather_smem_kernel(const void* A, const void* B, int qa, int qb, int n_leaves, int leaves_per_group,
+                   const double* weights, const uint32_t* packed, long long n_req, int req_per_cta,
+                   double2* partial) {
+  using V = typename Cx<R>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int na = 1 << qa, nb = 1 << qb;
+  const int pair = na + nb;  // elements per buffer
+  V* buf0 = reinterpret_cast<V*>(smem_raw);
+  V* buf1 = buf0 + pair;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const long long r0 = (long long)blockIdx.x * req_per_cta;
+  const int j0 = blockIdx.y * leaves_per_group;
+  const int j1 = min(n_leaves, j0 + leaves_per_group);
+
+  uint32_t idx[RPT];
+  double acc_re[RPT], acc_im[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const long long i = r0 + tid + (long long)r * nt;
+    idx[r] = (i < n_req && (tid + r * nt) < req_per_cta) ? packed[i] : 0xffffffffu;
+    acc_re[r] = 0.0;
+    acc_im[r] = 0.0;
+  }
+  const V* gA = reinterpret_cast<const V*>(A);
+  const V* gB = reinterpret_cast<const V*>(B);
+  constexpr int PER16 = 16 / sizeof(V);  // elements per 16-byte chunk
+  auto issue = [&](int j, V* dst) {
+    const V* a = gA + (long long)j * na;
+    const V* b = gB + (long long)j * nb;
+    for (int c = tid; c < na / PER16; c += nt) cp_async16(dst + c * PER16, a + c * PER16);
+    for (int c = tid; c < nb / PER16; c += nt) cp_async16(dst + na + c * PER16, b + c * PER16);
+    cp_async_commit();
+  };
+  if (j0 < j1) issue(j0, buf0);
+  const uint32_t amask = (uint32_t)na - 1;
+  for (int j = j0; j < j1; ++j) {
+    V* cur = ((j - j0) & 1) ? buf1 : buf0;
+    V* nxt = ((j - j0) & 1) ? buf0 : buf1;
+    cp_async_wait_all();
+    __syncthreads();  // leaf j resident; everyone done with leaf j-1's buffer
+    if (j + 1 < j1) issue(j + 1, nxt);
+    const double w = weights[j];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      if (idx[r] == 0xffffffffu) continue;
+      const V x = cur[idx[r] & amask];
+      const V y = cur[na + (idx[r] >> qa)];
+      const double xr = x.x, xi = x.y, yr = y.x, yi = y.y;
+      double pr = xr * yr - xi * yi, pi = xr * yi + xi * yr;
+      if (w != 1.0) pr *= w, pi *= w;
+      acc_re[r] += pr;
+      acc_im[r] += pi;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const long long i = r0 + tid + (long long)r * nt;
+    if (idx[r] != 0xffffffffu)
+      partial[(long long)blockIdx.y * n_req + i] = make_double2(acc_re[r], acc_im[r]);
+  }
+}
+
+}  // namespace gs

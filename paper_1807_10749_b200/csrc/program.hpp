@@ -62,6 +62,7 @@ struct PassPlan {
 
 struct Level {
   int k_lo = 0, k_hi = 0;  // cross digits [k_lo, k_hi) introduced at this level
+  std::vector<uint64_t> packed;  // mixed-radix level digit -> packed nibbles
   std::vector<HostOp> ops[2];
   std::vector<PassPlan> passes[2];
 };
