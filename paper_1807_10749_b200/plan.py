@@ -112,8 +112,17 @@ def split_requests(n_qubits: int, block_a, block_b, indices):
     for block in (block_a, block_b):
         width = len(block)
         local = np.zeros(idx.shape, dtype=np.int64)
-        for j, q in enumerate(block):
-            local |= ((idx >> (n_qubits - 1 - q)) & 1) << (width - 1 - j)
+        # runs of consecutive qubits are runs of consecutive bits: one shift+mask each
+        j = 0
+        while j < width:
+            k = j
+            while k + 1 < width and block[k + 1] == block[k] + 1:
+                k += 1
+            run = k - j + 1
+            src = n_qubits - 1 - block[k]  # global bit of the run's lowest bit
+            dst = width - 1 - k            # local bit of the run's lowest bit
+            local |= ((idx >> src) & ((1 << run) - 1)) << dst
+            j = k + 1
         halves.append(local)
     return halves[0], halves[1]
 
