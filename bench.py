@@ -44,7 +44,7 @@ METRIC = "Feynman paths/sec (whole box)"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--window", type=int, default=0, help="prefixes per GPU per step (0 = auto)")
@@ -74,32 +74,55 @@ def describe(name, plan, window, n_req):
 # clocks sampled during the timed region
 
 class ClockSampler:
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampler started before the timed region; summary() keeps the
+    samples whose timestamps fall inside [t0, t1] (the nearest one if none)."""
+
+    QUERY = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_ms: int = 20):
         self.gpu = gpu_index
+        self.period = period_ms
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            deadline = time.time() + 10
+            while not self.rows and time.time() < deadline:  # wait for the first sample
+                time.sleep(0.02)
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+        import datetime
 
-    def __exit__(self, *exc):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = time.time()
+            self.rows.append((ts, f[1:]))
+
+    def mark(self, begin: bool):
+        if begin:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+            time.sleep(2 * self.period / 1000.0)
+
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -109,14 +132,26 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        inside = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+        how = "during timed region"
+        if not inside:
+            mid = 0.5 * (self.t0 + self.t1) if self.t0 and self.t1 else time.time()
+            inside = [min(self.rows, key=lambda tr: abs(tr[0] - mid))[1]]
+            how = "nearest sample to the timed region"
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in inside if num(r[1]) is not None]
+        mx = [num(r[2]) for r in inside if num(r[2]) is not None]
+        reasons = sorted({self.NAMES[i] for r in inside for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(inside), "sampling": how}
 
 
 # ---------------------------------------------------------------------------
@@ -238,13 +273,16 @@ def main():
         dist.barrier()
     stats = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for s in range(args.steps):
-            step(args.warmup + s, stats)
-        e1.record(stream)
-        torch.cuda.synchronize()
+    clk = ClockSampler(local).start()
+    torch.cuda.synchronize()
+    clk.mark(True)
+    e0.record(stream)
+    for s in range(args.steps):
+        step(args.warmup + s, stats)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk.mark(False)
+    clk.stop()
     ms = e0.elapsed_time(e1)
     if world > 1:
         dist.barrier()
@@ -358,7 +396,14 @@ def main():
 
 
 def main_reference(args):
-    """Reference arm: the reference algorithm (oracle port) on all host cores, rank 0 only."""
+    """Reference arm: the reference algorithm (oracle port of run_batched) on all host cores.
+
+    A timed step is the workload's natural unit on every core: each process
+    evaluates one retained prefix with all of its branches (the reference's
+    per-prefix job, orchestrator.py:133-159, on its batched engine).  Warm-up
+    steps only import and run one path on one process (they are untimed).
+    Rank 0 alone runs under torchrun.
+    """
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -370,15 +415,15 @@ def main_reference(args):
     name = args.config
     circ, plan, req, pre_all = configs.build(name)
     procs = args.cpu_procs or min(os.cpu_count() or 1, 64)
-    per_step = procs  # one prefix (all its branches) per process per step
     pool = mp.get_context("fork").Pool(procs)
+    for s in range(args.warmup):
+        pool.map(_cpu_job, [(name, pre_all[s:s + 1], 64)])
     times, paths = [], 0
-    for s in range(args.warmup + args.steps):
-        sample = pre_all[s * per_step:(s + 1) * per_step]
+    for s in range(args.steps):
+        sample = pre_all[(s * procs) % max(1, pre_all.size - procs):][:procs]
         wall, _, used = cpu_reference(name, sample, req.size, procs, pool)
-        if s >= args.warmup:
-            times.append(wall)
-            paths += sample.size * plan.branch_space
+        times.append(wall)
+        paths += sample.size * plan.branch_space
     pool.close()
     total = sum(times)
     value = paths / total
@@ -388,10 +433,11 @@ def main_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "impl": "reference",
         "dtype": "c64 (numpy complex64 states, complex128 accumulation)",
         "data": "synthetic: reference-generator circuit (seed 0), challenge_indices(seed 12345)",
-        "config": {"workload": describe(name, plan, per_step, req.size) + " (CPU: one prefix per process)",
+        "config": {"workload": describe(name, plan, procs, req.size) + " (CPU: one prefix per process)",
                    "parallelism": f"{procs} forked CPU processes"},
         "cpu_baseline": {"value": value, "unit": "paths/s", "cores": procs, "kind": "port",
-                         "sample": f"{per_step} prefixes x {plan.branch_space} branches per step"},
+                         "sample": f"{procs} prefixes x {plan.branch_space} branches per step "
+                                   f"(numpy restatement of reference run_batched, oracle/)"},
         "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

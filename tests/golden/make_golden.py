@@ -288,9 +288,11 @@ def full_state_cases():
     save("cfg2_full", requests=req, exact=exact, seconds=time.time() - t)
 
 
-def heavy_cases():
+def heavy_cases(which=("cfg5", "cfg5f")):
     """cfg5 windows at 28|28 (hours of CPU; 2 GiB half-states)."""
     for name, fs in (("cfg5", False), ("cfg5f", True)):
+        if name not in which:
+            continue
         base = gen(7, 8, 40, "v1")
         circ = fsim_variant(base) if fs else base
         if fs:
@@ -318,7 +320,7 @@ if __name__ == "__main__":
     ap.add_argument("--only", default="")
     args = ap.parse_args()
     if args.heavy:
-        heavy_cases()
+        heavy_cases(tuple(args.only.split(",")) if args.only else ("cfg5", "cfg5f"))
         sys.exit(0)
     steps = args.only.split(",") if args.only else ["circuits", "small", "configs", "full"]
     if "circuits" in steps:
