@@ -58,7 +58,7 @@ def parse():
 
 
 DEFAULT_WINDOW = {"cfg1": 16, "cfg1v2": 32, "cfg2": 32768, "cfg2v2": 32768, "cfg2h": 2048,
-                  "cfg3": 256, "cfg3v2": 128, "cfg4": 8, "cfg4v2": 4, "cfg5": 1, "cfg5v2": 1, "cfg5f": 1}
+                  "cfg3": 256, "cfg3v2": 128, "cfg4": 32, "cfg4v2": 16, "cfg5": 1, "cfg5v2": 1, "cfg5f": 1}
 
 
 def describe(name, plan, window, n_req):
