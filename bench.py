@@ -241,7 +241,10 @@ def main():
     for kv in args.opt:
         key, val = kv.split("=")
         eng.set_option(key, int(val))
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) stream shared by torch and the engine: the CUDA events
+    # below then bracket exactly the engine's launches
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
     prog = lowered(circ, plan.cut)
     eng.load_program(prog)

@@ -1014,7 +1014,11 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
   } else {
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
-    budget = 0.80 * (double)fr - 1.5e9;
+    // level buffers this context already holds are reused, so they count as free
+    double held = 0;
+    for (auto* v : {&c.lvl_a, &c.lvl_b})
+      for (const DevBuf& b : *v) held += (double)b.bytes;
+    budget = 0.80 * ((double)fr + held) - 1.5e9;
     budget = std::max(budget, 4.0 * pair);
   }
   // largest uniform cap with sum_l min(bound_l, cap) * pair <= budget
@@ -1024,7 +1028,10 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
     return s;
   };
   double lo = 1, hi = (double)c.max_chunk;
-  if (need(1) > budget) throw GsError(GS_ERR_NOMEM, "device memory budget below one node per level");
+  if (need(1) > budget)
+    throw GsError(GS_ERR_NOMEM, "device memory budget below one node per level (need " +
+                                    std::to_string(need(1) / 1e9) + " GB for " + std::to_string(D + 1) +
+                                    " levels, budget " + std::to_string(budget / 1e9) + " GB)");
   while (hi - lo > 0.5) {
     double mid = std::floor((lo + hi + 1) / 2);
     if (need(mid) <= budget) lo = mid; else hi = mid - 1;
@@ -1041,6 +1048,11 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
     cudaEvent_t e;
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c.lvl_event.push_back(e);
+  }
+  // release oversized buffers first so growing one level cannot overshoot the budget
+  for (int l = 0; l <= D; ++l) {
+    if (c.lvl_a[l].bytes > (size_t)c.cap[l] * ((size_t)1 << p.q[0]) * c.esize()) c.lvl_a[l].release();
+    if (c.lvl_b[l].bytes > (size_t)c.cap[l] * ((size_t)1 << p.q[1]) * c.esize()) c.lvl_b[l].release();
   }
   for (int l = 0; l <= D; ++l) {
     c.lvl_a[l].ensure((size_t)c.cap[l] * ((size_t)1 << p.q[0]) * c.esize());
