@@ -136,6 +136,9 @@ struct Ctx {
   int kernel_version = 2;
   int hoist = 1;  // move digit-independent ops above branch points
   int smem_gather = 1;
+  int grouped_enabled = 1;
+  bool grouped_leaf = false;
+  DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
   int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
   // requests
@@ -502,10 +505,20 @@ static uint64_t pack_level_digits(const Program& p, int l, int64_t v);
 static void schedule_program(Ctx& c) {
   Program& p = c.prog;
   c.host_devops.clear();
+  // Leaf states go to the grouped path-minor layout when the gather reads them
+  // from HBM (half-states too large for the shared-memory gather).
+  {
+    const size_t pair_bytes = (((size_t)1 << p.q[0]) + ((size_t)1 << p.q[1])) * c.esize();
+    c.grouped_leaf = c.kernel_version == 2 && c.grouped_enabled && 2 * pair_bytes > 200 * 1024 &&
+                     std::min(p.q[0], p.q[1]) >= 12;
+  }
+  const int D = (int)p.levels.size() - 1;
   for (size_t l = 0; l < p.levels.size(); ++l) {
     Level& L = p.levels[l];
     for (int side = 0; side < 2; ++side) {
-      L.passes[side] = schedule_passes(L.ops[side], p.q[side], c.kmax(), c.low_bits, true);
+      const int kcap = ((int)l == D && c.grouped_leaf) ? c.kmax() - 2 : c.kmax();
+      L.passes[side] = schedule_passes(L.ops[side], p.q[side], kcap, c.low_bits, true);
+      if ((int)l == D && c.grouped_leaf) L.passes[side].back().grouped_store = true;
       for (PassPlan& pp : L.passes[side]) {
         pp.dev_op_offset = (int64_t)c.host_devops.size();
         std::vector<int> tpos(p.q[side], -1);
@@ -577,7 +590,16 @@ static void schedule_program(Ctx& c) {
             std::vector<int> tbits;
             for (int j = 0; j < pp.K; ++j)
               if (j >= pp.k || rpos[j] < 0) tbits.push_back(j);
-            if (!hbm_stage) {
+            if (pp.grouped_store && si + 1 == pp.stages.size()) {
+              // grouped store: slot bits on the lowest lanes -> 4 leaves x 8 amplitudes
+              // = 256 contiguous bytes per warp store
+              std::vector<int> slot_first;
+              for (int j : tbits)
+                if (j >= pp.k) slot_first.push_back(j);
+              for (int j : tbits)
+                if (j < pp.k) slot_first.push_back(j);
+              tbits = slot_first;
+            } else if (!hbm_stage) {
               const int nclass = (c.precision == GS_C64) ? 4 : 3;
               std::vector<int> lanes, rest;
               std::vector<char> used_class(nclass, 0);
@@ -822,6 +844,8 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
   a.tiles_log = q - pp.k;
   a.init_zero = init_zero ? 1 : 0;
   a.n_hi = 1 << (pp.k - a.c);
+  a.out_group_log = pp.grouped_store ? 2 : 0;
+  if (pp.grouped_store && pp.K - pp.k != 2) throw GsError(GS_ERR_ARG, "grouped store needs 2 slot bits");
   for (int j = 0; j < pp.k; ++j) a.lbits[j] = pp.lbits[j];
   for (int j = 0; j < (int)pp.gbits.size(); ++j) a.gbits[j] = pp.gbits[j];
   const int threads = 1 << (a.K - pp.M);
@@ -876,8 +900,9 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
   for (int side = 0; side < 2; ++side) {
     bool first = true;
     for (const PassPlan& pp : L.passes[side]) {
+      void* out = pp.grouped_store ? c.leaf_out[side].p : dsts[side];
       if (c.kernel_version == 2 && pp.M > 0)
-        launch_pass2<R>(c, side, pp, first ? srcs[side] : dsts[side], dsts[side],
+        launch_pass2<R>(c, side, pp, first ? srcs[side] : dsts[side], out,
                         first ? parent : nullptr, digit, n, root && first);
       else
         launch_pass<R>(c, side, pp, first ? srcs[side] : dsts[side], dsts[side],
@@ -919,7 +944,21 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   c.d_partial.ensure((size_t)groups * nreq * sizeof(double2));
   const int qa = c.prog.q[0], qb = c.prog.q[1];
   const size_t pair_bytes = ((size_t)1 << qa) * c.esize() + ((size_t)1 << qb) * c.esize();
-  if (c.smem_gather && 2 * pair_bytes <= 200 * 1024 && qa + qb <= 31 && qa >= 2 && qb >= 2) {
+  if (c.grouped_leaf) {
+    const int64_t ng = (n + 3) / 4;
+    int64_t gy = std::max<int64_t>(1, (148 * 16) / std::max<int64_t>(1, xblocks));
+    gy = std::min<int64_t>(gy, ng);
+    gy = std::min<int64_t>(gy, std::max<int64_t>(1, (256LL << 20) / (16 * std::max<int64_t>(1, nreq))));
+    const int64_t per_y = (ng + gy - 1) / gy;
+    gy = (ng + per_y - 1) / per_y;
+    c.d_partial.ensure((size_t)gy * nreq * sizeof(double2));
+    gather_grouped_kernel<R><<<dim3((unsigned)xblocks, (unsigned)gy), threads, 0, c.stream>>>(
+        c.leaf_out[0].p, c.leaf_out[1].p, 1LL << qa, 1LL << qb, (int)n, (int)per_y,
+        reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const int32_t*>(c.d_ia.p),
+        reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
+    launch_check("gather_grouped_kernel", xblocks * gy, threads, 0);
+    groups = gy;
+  } else if (c.smem_gather && 2 * pair_bytes <= 200 * 1024 && qa + qb <= 31 && qa >= 2 && qb >= 2) {
     // shared-memory gather: whole leaf pairs staged per CTA, requests in registers
     constexpr int RPT = 20, NT = 512;
     const int64_t req_per_cta = (int64_t)RPT * NT;
@@ -1062,6 +1101,10 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
     c.lvl_stage[l].ensure(c.cap[l] * 12 + 16);
   }
   if (!c.weights_event) CK(cudaEventCreateWithFlags(&c.weights_event, cudaEventDisableTiming));
+  if (c.grouped_leaf) {
+    const size_t slots = (size_t)((c.cap[D] + 3) / 4) * 4;
+    for (int side = 0; side < 2; ++side) c.leaf_out[side].ensure(slots * ((size_t)1 << p.q[side]) * c.esize());
+  }
 }
 
 template <typename R>
@@ -1197,6 +1240,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "hoist") {
       c.hoist = value ? 1 : 0;
       if (c.have_prog) throw GsError(GS_ERR_STATE, "set hoist before gs_load_program");
+    } else if (k == "grouped_leaf") {
+      c.grouped_enabled = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "smem_gather") {
       c.smem_gather = value ? 1 : 0;
     } else if (k == "reg_bits") {

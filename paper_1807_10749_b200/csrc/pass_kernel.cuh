@@ -388,7 +388,9 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
 
   // last stage: registers -> HBM
   if (!active) return;
-  V* d = reinterpret_cast<V*>(a.dst) + slot * a.state_elems;
+  const int G = a.out_group_log;  // grouped path-minor leaf layout for the gather
+  V* d = reinterpret_cast<V*>(a.dst) +
+         (G ? (((slot >> G) * a.state_elems) << G) + (slot & ((1 << G) - 1)) : slot * a.state_elems);
   const R sc = (R)a.store_scale;
   const bool do_scale = a.store_scale != 1.0;
   long long gstep[M];
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
     if (n) o ^= gstep[ctz_c(n)];
     V x = v[n ^ (n >> 1)];
     if (do_scale) x.x *= sc, x.y *= sc;
-    d[o] = x;
+    d[o << G] = x;
   }
 }
 

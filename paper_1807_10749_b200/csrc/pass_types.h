@@ -62,6 +62,7 @@ struct Pass2Args {
   int tiles_log;
   int init_zero;
   int n_hi;
+  int out_group_log;  // > 0: store leaf states grouped path-minor, [slot >> G][x][slot & (2^G-1)]
   int lbits[16];
   int gbits[40];
 };

@@ -58,6 +58,7 @@ struct PassPlan {
   int K = 0;                    // tile bits incl. slot bits (v2 kernel)
   int64_t dev_stage_offset = 0; // into the device stage array
   double store_scale = 1.0;     // power of two applied on store
+  bool grouped_store = false;   // leaf level, last pass: grouped path-minor store
 };
 
 struct Level {
