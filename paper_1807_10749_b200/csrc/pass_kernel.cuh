@@ -323,9 +323,11 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
   V v[E];
   const PStage* st = a.stages;
   int tb = thread_tile_base<M>(st, tid, nthr_bits);
-  const long long slot = (group << (K - kq)) | (tb >> kq);
-  const bool active = slot < a.n_states;
-  const unsigned long long node_digits = (a.digits && active) ? a.digits[slot] : 0ull;
+  // slot (which state of the CTA) is a function of the stage's thread mapping:
+  // recomputed after every exchange, with the digits that belong to it
+  long long slot = (group << (K - kq)) | (tb >> kq);
+  bool active = slot < a.n_states;
+  unsigned long long node_digits = (a.digits && active) ? a.digits[slot] : 0ull;
 
   // stage 0: HBM -> registers (register bits are high tile bits: lanes contiguous)
   {
@@ -372,6 +374,11 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
     __syncthreads();
     st = a.stages + s;
     tb = thread_tile_base<M>(st, tid, nthr_bits);
+    if (K > kq) {
+      slot = (group << (K - kq)) | (tb >> kq);
+      active = slot < a.n_states;
+      node_digits = (a.digits && active) ? a.digits[slot] : 0ull;
+    }
     {
       int sstep[M];
 #pragma unroll
