@@ -131,6 +131,9 @@ struct Ctx {
   std::vector<double> host_params;   // 4 per param: rs, t, sn, mode
   std::vector<int32_t> host_pxtable;
   std::vector<int> pxbase[2];        // per cross gate and side: pxtable base
+  std::vector<uint16_t> host_tbtab;  // [stage][256] thread -> tile-index base
+  std::vector<uint32_t> host_gofftab;  // per pass [2^k] tile index -> state offset
+  DevBuf d_tbtab, d_gofftab;
   std::vector<PStage> host_pstages;
   double kfinal[2][2] = {{1, 0}, {1, 0}};  // per block: true = stored * K
   int kernel_version = 2;
@@ -560,6 +563,8 @@ static void schedule_program(Ctx& c) {
   c.pxbase[0].assign(p.n_cross, -1);
   c.pxbase[1].assign(p.n_cross, -1);
   c.host_pstages.clear();
+  c.host_tbtab.clear();
+  c.host_gofftab.clear();
   for (int side = 0; side < 2; ++side) {
     double kre = 1.0, kim = 0.0;  // true amplitude = stored * K
     for (size_t l = 0; l < p.levels.size(); ++l) {
@@ -574,6 +579,12 @@ static void schedule_program(Ctx& c) {
         pp.K = std::max(pp.k, std::min(c.kmax(), pp.M + 8));
         pp.stages = schedule_stages(pp, pp.M);
         pp.dev_stage_offset = (int64_t)c.host_pstages.size();
+        pp.goff_offset = (int64_t)c.host_gofftab.size();
+        for (int t = 0; t < (1 << pp.k); ++t) {
+          uint32_t g = 0;
+          for (int j = 0; j < pp.k; ++j) g |= (uint32_t)((t >> j) & 1) << pp.lbits[j];
+          c.host_gofftab.push_back(g);
+        }
         std::vector<int> tpos(p.q[side], -1);
         for (int j = 0; j < (int)pp.lbits.size(); ++j) tpos[pp.lbits[j]] = j;
         for (const StagePlan& sp : pp.stages) {
@@ -615,6 +626,14 @@ static void schedule_program(Ctx& c) {
               tbits.insert(tbits.end(), rest.begin(), rest.end());
             }
             for (int j = 0; j < (int)tbits.size() && j < 16; ++j) ps.tb[j] = (int8_t)tbits[j];
+            // thread -> tile-index base for this stage (row of 256 in tbtab)
+            const int nthr = 1 << (pp.K - pp.M);
+            for (int t = 0; t < 256; ++t) {
+              int tbv = 0;
+              if (t < nthr)
+                for (int j = 0; j < pp.K - pp.M; ++j) tbv |= ((t >> j) & 1) << tbits[j];
+              c.host_tbtab.push_back((uint16_t)tbv);
+            }
           }
           ps.op_begin = (int32_t)c.host_prims.size();
           for (const HostOp& op : sp.ops) {
@@ -673,6 +692,8 @@ static void upload_program(Ctx& c) {
   upload(c, c.d_prims, c.host_prims);
   upload(c, c.d_pstages, c.host_pstages);
   upload(c, c.d_pxtable, c.host_pxtable);
+  upload(c, c.d_tbtab, c.host_tbtab);
+  upload(c, c.d_gofftab, c.host_gofftab);
   if (c.precision == GS_C64) {
     std::vector<float> f(c.host_params.begin(), c.host_params.end());
     upload(c, c.d_params, f);
@@ -845,6 +866,10 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
   a.init_zero = init_zero ? 1 : 0;
   a.n_hi = 1 << (pp.k - a.c);
   a.out_group_log = pp.grouped_store ? 2 : 0;
+  a.stage0 = (int)pp.dev_stage_offset;
+  a.tbtab = reinterpret_cast<const uint16_t*>(c.d_tbtab.p);
+  a.gofftab = reinterpret_cast<const uint32_t*>(c.d_gofftab.p) + pp.goff_offset;
+  if (q > 31) throw GsError(GS_ERR_ARG, "half-states beyond 2^31 amplitudes are not supported");
   if (pp.grouped_store && pp.K - pp.k != 2) throw GsError(GS_ERR_ARG, "grouped store needs 2 slot bits");
   for (int j = 0; j < pp.k; ++j) a.lbits[j] = pp.lbits[j];
   for (int j = 0; j < (int)pp.gbits.size(); ++j) a.gbits[j] = pp.gbits[j];

@@ -289,11 +289,18 @@ __device__ __forceinline__ void apply_prims(V (&v)[1 << M], const Pass2Args& a, 
   }
 }
 
-template <int M>
-__device__ __forceinline__ int thread_tile_base(const PStage* st, int tid, int nthr_bits) {
-  int t = 0;
-  for (int j = 0; j < nthr_bits; ++j) t |= ((tid >> j) & 1) << st->tb[j];
-  return t;
+// shared-memory element store/load by 32-bit shared-window byte address
+__device__ __forceinline__ void sts(uint32_t a, float2 x) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x.x), "f"(x.y) : "memory");
+}
+__device__ __forceinline__ void sts(uint32_t a, double2 x) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x.x), "d"(x.y) : "memory");
+}
+__device__ __forceinline__ void lds(uint32_t a, float2& x) {
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x.x), "=f"(x.y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void lds(uint32_t a, double2& x) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x.x), "=d"(x.y) : "r"(a) : "memory");
 }
 
 template <typename R, int M>
@@ -302,27 +309,21 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
   constexpr int E = 1 << M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* tile = reinterpret_cast<V*>(smem_raw);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const int K = a.K;
-  const int nthr_bits = K - M;
   const int tid = threadIdx.x;
 
   const long long group = (long long)(blockIdx.x >> a.tiles_log);
   const int tile_id = blockIdx.x & ((1 << a.tiles_log) - 1);
-  long long base = 0;
-  for (int j = 0; j < a.tiles_log; ++j) base |= (long long)((tile_id >> j) & 1) << a.gbits[j];
+  uint32_t base = 0;  // state bits fixed by the tile id (q <= 31)
+  for (int j = 0; j < a.tiles_log; ++j) base |= (uint32_t)((tile_id >> j) & 1) << a.gbits[j];
   const int kq = a.kq;
   const int kqmask = (1 << kq) - 1;
 
-  // global offset of a tile index: linear in its bits (tile bit j -> state bit lbits[j])
-  auto goff = [&](int t) {
-    long long o = 0;
-    for (int j = 0; j < kq; ++j) o |= (long long)((t >> j) & 1) << a.lbits[j];
-    return o;
-  };
-
   V v[E];
   const PStage* st = a.stages;
-  int tb = thread_tile_base<M>(st, tid, nthr_bits);
+  // per-stage thread -> tile-index base, precomputed by the host
+  int tb = a.tbtab[a.stage0 * 256 + tid];
   // slot (which state of the CTA) is a function of the stage's thread mapping:
   // recomputed after every exchange, with the digits that belong to it
   long long slot = (group << (K - kq)) | (tb >> kq);
@@ -331,10 +332,10 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
 
   // stage 0: HBM -> registers (register bits are high tile bits: lanes contiguous)
   {
-    long long gstep[M];
+    uint32_t gstep[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) gstep[i] = 1LL << a.lbits[st->rb[i]];
-    long long o = base | goff(tb & kqmask);
+    for (int i = 0; i < M; ++i) gstep[i] = 1u << a.lbits[st->rb[i]];
+    uint32_t o = base | a.gofftab[tb & kqmask];
     if (a.init_zero) {
 #pragma unroll
       for (int n = 0; n < E; ++n) {
@@ -345,11 +346,11 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
       }
     } else if (active) {
       const long long ss = a.parent ? (long long)a.parent[slot] : slot;
-      const V* s = reinterpret_cast<const V*>(a.src) + ss * a.state_elems;
+      const V* sp = reinterpret_cast<const V*>(a.src) + ss * a.state_elems;
 #pragma unroll
       for (int n = 0; n < E; ++n) {
         if (n) o ^= gstep[ctz_c(n)];
-        v[n ^ (n >> 1)] = s[o];
+        v[n ^ (n >> 1)] = sp[o];
       }
     } else {
 #pragma unroll
@@ -361,33 +362,33 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
   for (int s = 1; s < a.n_stages; ++s) {
     if (s > 1) __syncthreads();
     {
-      int sstep[M];
+      uint32_t sstep[M];
 #pragma unroll
-      for (int i = 0; i < M; ++i) sstep[i] = swz<V>(1 << st->rb[i]);
-      int addr = swz<V>(tb);
+      for (int i = 0; i < M; ++i) sstep[i] = (uint32_t)swz<V>(1 << st->rb[i]) * sizeof(V);
+      uint32_t off = (uint32_t)swz<V>(tb) * sizeof(V);
 #pragma unroll
       for (int n = 0; n < E; ++n) {
-        if (n) addr ^= sstep[ctz_c(n)];
-        tile[addr] = v[n ^ (n >> 1)];
+        if (n) off ^= sstep[ctz_c(n)];
+        sts(sbase + off, v[n ^ (n >> 1)]);
       }
     }
     __syncthreads();
     st = a.stages + s;
-    tb = thread_tile_base<M>(st, tid, nthr_bits);
+    tb = a.tbtab[(a.stage0 + s) * 256 + tid];
     if (K > kq) {
       slot = (group << (K - kq)) | (tb >> kq);
       active = slot < a.n_states;
       node_digits = (a.digits && active) ? a.digits[slot] : 0ull;
     }
     {
-      int sstep[M];
+      uint32_t sstep[M];
 #pragma unroll
-      for (int i = 0; i < M; ++i) sstep[i] = swz<V>(1 << st->rb[i]);
-      int addr = swz<V>(tb);
+      for (int i = 0; i < M; ++i) sstep[i] = (uint32_t)swz<V>(1 << st->rb[i]) * sizeof(V);
+      uint32_t off = (uint32_t)swz<V>(tb) * sizeof(V);
 #pragma unroll
       for (int n = 0; n < E; ++n) {
-        if (n) addr ^= sstep[ctz_c(n)];
-        v[n ^ (n >> 1)] = tile[addr];
+        if (n) off ^= sstep[ctz_c(n)];
+        lds(sbase + off, v[n ^ (n >> 1)]);
       }
     }
     apply_prims<M>(v, a, st->op_begin, st->op_end, tb, base, node_digits, tile, st);
@@ -400,16 +401,16 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
          (G ? (((slot >> G) * a.state_elems) << G) + (slot & ((1 << G) - 1)) : slot * a.state_elems);
   const R sc = (R)a.store_scale;
   const bool do_scale = a.store_scale != 1.0;
-  long long gstep[M];
+  uint32_t gstep[M];
 #pragma unroll
-  for (int i = 0; i < M; ++i) gstep[i] = 1LL << a.lbits[st->rb[i]];
-  long long o = base | goff(tb & kqmask);
+  for (int i = 0; i < M; ++i) gstep[i] = (1u << a.lbits[st->rb[i]]) << G;
+  uint32_t o = (base | a.gofftab[tb & kqmask]) << G;
 #pragma unroll
   for (int n = 0; n < E; ++n) {
     if (n) o ^= gstep[ctz_c(n)];
     V x = v[n ^ (n >> 1)];
     if (do_scale) x.x *= sc, x.y *= sc;
-    d[o << G] = x;
+    d[o] = x;
   }
 }
 

@@ -63,6 +63,9 @@ struct Pass2Args {
   int init_zero;
   int n_hi;
   int out_group_log;  // > 0: store leaf states grouped path-minor, [slot >> G][x][slot & (2^G-1)]
+  int stage0;                 // global index of the pass's first stage (tbtab rows)
+  const uint16_t* tbtab;      // [stage][256] thread -> tile-index base
+  const uint32_t* gofftab;    // [2^kq] tile index -> state offset of the pass
   int lbits[16];
   int gbits[40];
 };

@@ -57,6 +57,7 @@ struct PassPlan {
   int M = 0;                    // register bits per stage
   int K = 0;                    // tile bits incl. slot bits (v2 kernel)
   int64_t dev_stage_offset = 0; // into the device stage array
+  int64_t goff_offset = 0;      // into the tile-index -> state-offset table
   double store_scale = 1.0;     // power of two applied on store
   bool grouped_store = false;   // leaf level, last pass: grouped path-minor store
 };
