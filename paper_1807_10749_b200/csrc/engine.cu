@@ -591,6 +591,14 @@ static void schedule_program(Ctx& c) {
           PStage ps{};
           std::vector<int> rpos(pp.k, -1);
           for (int i = 0; i < (int)sp.rb.size(); ++i) ps.rb[i] = (int8_t)sp.rb[i], rpos[sp.rb[i]] = i;
+          {  // swizzled shared-tile byte step per register bit (pass_kernel.cuh swz)
+            const int lb = c.precision == GS_C64 ? 4 : 3;
+            for (int i = 0; i < (int)sp.rb.size(); ++i) {
+              const uint32_t t = 1u << sp.rb[i];
+              const uint32_t z = t ^ (((t >> lb) ^ (t >> (2 * lb)) ^ (t >> (3 * lb)) ^ (t >> (4 * lb))) & ((1u << lb) - 1));
+              ps.sstep[i] = z * (uint32_t)c.esize();
+            }
+          }
           // thread-bit order over the tile bits (state bits then slot bits up to
           // the kernel's K); lanes are thread bits 0..4.  HBM stages keep the
           // lowest tile bits on the lanes; shared-memory-only stages pick lanes

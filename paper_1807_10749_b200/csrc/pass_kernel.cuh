@@ -352,10 +352,8 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
         if (n) o ^= gstep[ctz_c(n)];
         v[n ^ (n >> 1)] = sp[o];
       }
-    } else {
-#pragma unroll
-      for (int e = 0; e < E; ++e) v[e].x = v[e].y = R(0);
     }
+    // inactive slots keep unspecified values: ops never mix slots and they are never stored
   }
   apply_prims<M>(v, a, st->op_begin, st->op_end, tb, base, node_digits, tile, st);
 
@@ -364,7 +362,7 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
     {
       uint32_t sstep[M];
 #pragma unroll
-      for (int i = 0; i < M; ++i) sstep[i] = (uint32_t)swz<V>(1 << st->rb[i]) * sizeof(V);
+      for (int i = 0; i < M; ++i) sstep[i] = st->sstep[i];
       uint32_t off = (uint32_t)swz<V>(tb) * sizeof(V);
 #pragma unroll
       for (int n = 0; n < E; ++n) {
@@ -383,7 +381,7 @@ __global__ void __launch_bounds__(256) pass2_kernel(const __grid_constant__ Pass
     {
       uint32_t sstep[M];
 #pragma unroll
-      for (int i = 0; i < M; ++i) sstep[i] = (uint32_t)swz<V>(1 << st->rb[i]) * sizeof(V);
+      for (int i = 0; i < M; ++i) sstep[i] = st->sstep[i];
       uint32_t off = (uint32_t)swz<V>(tb) * sizeof(V);
 #pragma unroll
       for (int n = 0; n < E; ++n) {

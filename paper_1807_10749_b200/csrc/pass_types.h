@@ -13,6 +13,7 @@ struct PStage {
   int8_t rb[8];   // register bit i -> tile bit
   int8_t tb[16];  // thread-index bit j -> tile bit (lanes = j < 5)
   int32_t op_begin, op_end;
+  uint32_t sstep[8];  // byte step in the swizzled shared tile per register bit
 };
 
 // Flattened primitive of the v2 pass: one jump-table case per (kind, register
