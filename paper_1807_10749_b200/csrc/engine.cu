@@ -141,6 +141,7 @@ struct Ctx {
   int smem_gather = 1;
   int grouped_enabled = 1;
   bool grouped_leaf = false;
+  int group_log = 3;  // leaves per group = 2^group_log (64-byte request reads in c64)
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
   int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
@@ -519,7 +520,7 @@ static void schedule_program(Ctx& c) {
   for (size_t l = 0; l < p.levels.size(); ++l) {
     Level& L = p.levels[l];
     for (int side = 0; side < 2; ++side) {
-      const int kcap = ((int)l == D && c.grouped_leaf) ? c.kmax() - 2 : c.kmax();
+      const int kcap = ((int)l == D && c.grouped_leaf) ? c.kmax() - c.group_log : c.kmax();
       L.passes[side] = schedule_passes(L.ops[side], p.q[side], kcap, c.low_bits, true);
       if ((int)l == D && c.grouped_leaf) L.passes[side].back().grouped_store = true;
       for (PassPlan& pp : L.passes[side]) {
@@ -610,8 +611,8 @@ static void schedule_program(Ctx& c) {
             for (int j = 0; j < pp.K; ++j)
               if (j >= pp.k || rpos[j] < 0) tbits.push_back(j);
             if (pp.grouped_store && si + 1 == pp.stages.size()) {
-              // grouped store: slot bits on the lowest lanes -> 4 leaves x 8 amplitudes
-              // = 256 contiguous bytes per warp store
+              // grouped store: slot bits on the lowest lanes -> 2^G leaves x 2^(5-G)
+              // amplitudes = 256 contiguous bytes per warp store
               std::vector<int> slot_first;
               for (int j : tbits)
                 if (j >= pp.k) slot_first.push_back(j);
@@ -873,12 +874,13 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
   a.tiles_log = q - pp.k;
   a.init_zero = init_zero ? 1 : 0;
   a.n_hi = 1 << (pp.k - a.c);
-  a.out_group_log = pp.grouped_store ? 2 : 0;
+  a.out_group_log = pp.grouped_store ? c.group_log : 0;
   a.stage0 = (int)pp.dev_stage_offset;
   a.tbtab = reinterpret_cast<const uint16_t*>(c.d_tbtab.p);
   a.gofftab = reinterpret_cast<const uint32_t*>(c.d_gofftab.p) + pp.goff_offset;
   if (q > 31) throw GsError(GS_ERR_ARG, "half-states beyond 2^31 amplitudes are not supported");
-  if (pp.grouped_store && pp.K - pp.k != 2) throw GsError(GS_ERR_ARG, "grouped store needs 2 slot bits");
+  if (pp.grouped_store && pp.K - pp.k != c.group_log)
+    throw GsError(GS_ERR_ARG, "grouped store needs group_log slot bits");
   for (int j = 0; j < pp.k; ++j) a.lbits[j] = pp.lbits[j];
   for (int j = 0; j < (int)pp.gbits.size(); ++j) a.gbits[j] = pp.gbits[j];
   const int threads = 1 << (a.K - pp.M);
@@ -978,14 +980,16 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   const int qa = c.prog.q[0], qb = c.prog.q[1];
   const size_t pair_bytes = ((size_t)1 << qa) * c.esize() + ((size_t)1 << qb) * c.esize();
   if (c.grouped_leaf) {
-    const int64_t ng = (n + 3) / 4;
+    const int GL = c.group_log;
+    const int64_t ng = (n + (1 << GL) - 1) >> GL;
     int64_t gy = std::max<int64_t>(1, (148 * 16) / std::max<int64_t>(1, xblocks));
     gy = std::min<int64_t>(gy, ng);
     gy = std::min<int64_t>(gy, std::max<int64_t>(1, (256LL << 20) / (16 * std::max<int64_t>(1, nreq))));
     const int64_t per_y = (ng + gy - 1) / gy;
     gy = (ng + per_y - 1) / per_y;
     c.d_partial.ensure((size_t)gy * nreq * sizeof(double2));
-    gather_grouped_kernel<R><<<dim3((unsigned)xblocks, (unsigned)gy), threads, 0, c.stream>>>(
+    auto kern = GL == 3 ? gather_grouped_kernel<R, 3> : gather_grouped_kernel<R, 2>;
+    kern<<<dim3((unsigned)xblocks, (unsigned)gy), threads, 0, c.stream>>>(
         c.leaf_out[0].p, c.leaf_out[1].p, 1LL << qa, 1LL << qb, (int)n, (int)per_y,
         reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const int32_t*>(c.d_ia.p),
         reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
@@ -1135,7 +1139,8 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
   }
   if (!c.weights_event) CK(cudaEventCreateWithFlags(&c.weights_event, cudaEventDisableTiming));
   if (c.grouped_leaf) {
-    const size_t slots = (size_t)((c.cap[D] + 3) / 4) * 4;
+    const size_t gsz = (size_t)1 << c.group_log;
+    const size_t slots = (size_t)((c.cap[D] + gsz - 1) / gsz) * gsz;
     for (int side = 0; side < 2; ++side) c.leaf_out[side].ensure(slots * ((size_t)1 << p.q[side]) * c.esize());
   }
 }
@@ -1273,6 +1278,10 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "hoist") {
       c.hoist = value ? 1 : 0;
       if (c.have_prog) throw GsError(GS_ERR_STATE, "set hoist before gs_load_program");
+    } else if (k == "group_log") {
+      if (value != 2 && value != 3) throw GsError(GS_ERR_ARG, "group_log must be 2 or 3");
+      c.group_log = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "grouped_leaf") {
       c.grouped_enabled = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }

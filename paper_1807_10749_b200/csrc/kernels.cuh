@@ -306,46 +306,50 @@ gather_smem_kernel(const void* A, const void* B, int qa, int qb, int n_leaves, i
 
 // ---------------------------------------------------------------------------
 // Gather over grouped path-minor leaf states: leaf j of the chunk, amplitude x
-// lives at ((j >> 2) * 2^q + x) * 4 + (j & 3).  A request reads one 32-byte
-// sector per 4 leaves per half (complex64), all of it useful: 16 bytes per
-// (request, leaf), the algorithmic minimum of SURVEY.md §8d.
+// lives at ((j >> G) * 2^q + x) * 2^G + (j & (2^G - 1)).  A request reads
+// 2^G consecutive amplitudes per half and group (64 B for G = 3, complex64),
+// all of it useful: 16 bytes per (request, leaf), the algorithmic minimum of
+// SURVEY.md §8d.
 
-template <typename V> struct Quad { V v[4]; };
+template <typename V, int W> struct Group { V v[W]; };
 
-template <typename V> __device__ __forceinline__ Quad<V> load_quad(const V* p) {
-  Quad<V> q;
+template <typename V, int W> __device__ __forceinline__ Group<V, W> load_group(const V* p) {
+  Group<V, W> q;
   if constexpr (sizeof(V) == 8) {
-    const float4 lo = __ldg(reinterpret_cast<const float4*>(p));
-    const float4 hi = __ldg(reinterpret_cast<const float4*>(p) + 1);
-    q.v[0] = make_float2(lo.x, lo.y); q.v[1] = make_float2(lo.z, lo.w);
-    q.v[2] = make_float2(hi.x, hi.y); q.v[3] = make_float2(hi.z, hi.w);
+#pragma unroll
+    for (int k = 0; k < W / 2; ++k) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(p) + k);
+      q.v[2 * k] = make_float2(f.x, f.y);
+      q.v[2 * k + 1] = make_float2(f.z, f.w);
+    }
   } else {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) q.v[s] = __ldg(reinterpret_cast<const double2*>(p) + s);
+    for (int k = 0; k < W; ++k) q.v[k] = __ldg(reinterpret_cast<const double2*>(p) + k);
   }
   return q;
 }
 
-template <typename R>
+template <typename R, int GL>
 __global__ void __launch_bounds__(256)
 gather_grouped_kernel(const void* A, const void* B, long long a_elems, long long b_elems, int n_leaves,
                       int groups_per_y, const double* weights, const int32_t* ia, const int32_t* ib,
                       long long n_req, double2* partial) {
   using V = typename Cx<R>::T;
+  constexpr int W = 1 << GL;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_req) return;
-  const int n_groups = (n_leaves + 3) >> 2;
+  const int n_groups = (n_leaves + W - 1) >> GL;
   const int g0 = blockIdx.y * groups_per_y;
   const int g1 = min(n_groups, g0 + groups_per_y);
-  const V* pa = reinterpret_cast<const V*>(A) + 4LL * ia[i];
-  const V* pb = reinterpret_cast<const V*>(B) + 4LL * ib[i];
+  const V* pa = reinterpret_cast<const V*>(A) + ((long long)ia[i] << GL);
+  const V* pb = reinterpret_cast<const V*>(B) + ((long long)ib[i] << GL);
   double re = 0.0, im = 0.0;
   for (int g = g0; g < g1; ++g) {
-    const Quad<V> x = load_quad(pa + 4LL * g * a_elems);
-    const Quad<V> y = load_quad(pb + 4LL * g * b_elems);
+    const Group<V, W> x = load_group<V, W>(pa + (((long long)g * a_elems) << GL));
+    const Group<V, W> y = load_group<V, W>(pb + (((long long)g * b_elems) << GL));
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int j = 4 * g + s;
+    for (int s = 0; s < W; ++s) {
+      const int j = (g << GL) + s;
       if (j >= n_leaves) break;
       const double xr = x.v[s].x, xi = x.v[s].y, yr = y.v[s].x, yi = y.v[s].y;
       const double w = weights[j];
