@@ -17,9 +17,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libgridsim_b200.so")
-SOURCES = ["engine.cu", "pass_kernels.cu"]
-DEPS = ["engine.cu", "pass_kernels.cu", "kernels.cuh", "program.hpp", "pass_kernel.cuh",
-        "pass_kernel.h", "pass_types.h"]
+SOURCES = ["engine.cu", "pass_kernels.cu", "jit.cu"]
+DEPS = ["engine.cu", "pass_kernels.cu", "jit.cu", "jit.hpp", "jitgen.inc", "kernels.cuh", "program.hpp",
+        "pass_kernel.cuh", "pass_kernel.h", "pass_types.h"]
 
 NVCC_FLAGS = [
     "-O3",
@@ -30,7 +30,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-O2",
     "-Xptxas", "-v",
 ]
-LINK_FLAGS = ["-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a"]
+LINK_FLAGS = ["-shared", "-cudart", "static", "-gencode", "arch=compute_100a,code=sm_100a", "-ldl"]
 
 
 def nvcc_path() -> str:

@@ -10,8 +10,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -20,6 +22,7 @@
 
 #include "../../include/gridsim_b200.h"
 #include "kernels.cuh"
+#include "jit.hpp"
 #include "pass_kernel.h"
 #include "program.hpp"
 
@@ -145,6 +148,11 @@ struct Ctx {
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
   int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
+  int use_jit = 1;   // specialise passes at load time (NVRTC); interpreter otherwise
+  JitModule* jit = nullptr;
+  std::string jit_status = "off";
+  double jit_seconds = 0;
+  std::vector<size_t> jit_smem;
   // requests
   int64_t n_req = -1;
   DevBuf d_ia, d_ib, d_acc, d_partial;
@@ -172,6 +180,8 @@ struct Ctx {
     return k;
   }
 };
+
+#include "jitgen.inc"
 
 // ---------------------------------------------------------------------------
 // program loading
@@ -695,8 +705,66 @@ template <typename T> static void upload(Ctx& c, DevBuf& b, const std::vector<T>
   if (!v.empty()) CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
 }
 
+// Specialise every eligible pass (complex64, 5 register bits) into one NVRTC
+// module.  Failure keeps the interpreter kernels and records why.
+static void jit_program(Ctx& c) {
+  if (c.jit) {
+    jit_release(c.jit);
+    c.jit = nullptr;
+  }
+  c.jit_smem.clear();
+  for (Level& L : c.prog.levels)
+    for (int side = 0; side < 2; ++side)
+      for (PassPlan& pp : L.passes[side]) pp.jit_index = -1;
+  if (!c.use_jit || c.precision != GS_C64 || c.kernel_version != 2) {
+    c.jit_status = "off";
+    return;
+  }
+  std::string src = jitgen::prelude();
+  int n = 0;
+  std::vector<PassPlan*> order;
+  for (Level& L : c.prog.levels)
+    for (int side = 0; side < 2; ++side)
+      for (PassPlan& pp : L.passes[side]) {
+        if (pp.M != 5 || pp.stages.empty()) continue;
+        size_t smem = 0;
+        src += jitgen::pass_kernel(c, pp, n, smem);
+        c.jit_smem.push_back(smem);
+        order.push_back(&pp);
+        ++n;
+      }
+  if (n == 0) {
+    c.jit_status = "no eligible passes";
+    return;
+  }
+  if (const char* dump = std::getenv("GS_JIT_DUMP")) {  // diagnostics: write the generated module
+    if (FILE* f = std::fopen(dump, "w")) {
+      std::fwrite(src.data(), 1, src.size(), f);
+      std::fclose(f);
+    }
+  }
+  if (c.host_only) {
+    c.jit_status = "generated " + std::to_string(n) + " kernels (" + std::to_string(src.size()) +
+                   " bytes of source); not compiled on a host-only context";
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::string err;
+  c.jit = jit_compile(src, n, "gridsim_passes", err);
+  c.jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (!c.jit) {
+    c.jit_status = "interpreter (jit failed: " + err.substr(0, 300) + ")";
+    return;
+  }
+  for (int i = 0; i < n; ++i) order[i]->jit_index = i;
+  c.jit_status = "jit: " + std::to_string(n) + " pass kernels compiled in " + std::to_string(c.jit_seconds) + " s";
+}
+
 static void upload_program(Ctx& c) {
-  if (c.host_only) return;
+  if (c.host_only) {
+    jit_program(c);
+    return;
+  }
   upload(c, c.d_ops, c.host_devops);
   upload(c, c.d_prims, c.host_prims);
   upload(c, c.d_pstages, c.host_pstages);
@@ -716,6 +784,7 @@ static void upload_program(Ctx& c) {
   } else {
     upload(c, c.d_coef, c.prog.coef);
   }
+  jit_program(c);
 }
 
 // ---------------------------------------------------------------------------
@@ -829,12 +898,6 @@ static void launch_pass(Ctx& c, int side, const PassPlan& pp, const void* src, v
   launch_check("gate_pass_kernel", blocks, threads, smem);
 }
 
-static int ceil_log2(int64_t n) {
-  int b = 0;
-  while ((1LL << b) < n) ++b;
-  return b;
-}
-
 template <typename R, int M>
 static void launch_pass2_m(Ctx& c, const Pass2Args& a, int64_t blocks, int threads, size_t smem) {
   const cudaError_t e = launch_pass2_kernel(sizeof(R) == 4 ? 0 : 1, M, a, (unsigned)blocks, threads, smem, c.stream);
@@ -893,6 +956,24 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
   c.st.pass_bytes += 2.0 * (double)n_states * (double)(1LL << q) * (double)c.esize();
   c.st.pass_amp_updates += (double)n_states * (double)(1LL << q);
   if (c.host_only) return;
+  if (pp.jit_index >= 0 && c.jit) {
+    JArgs j{};
+    j.src = src;
+    j.dst = dst;
+    j.parent = parent;
+    j.digits = reinterpret_cast<const unsigned long long*>(digit);
+    j.params = c.d_params.p;
+    j.pxtable = reinterpret_cast<const int32_t*>(c.d_pxtable.p);
+    j.coefs = c.d_coef.p;
+    j.state_elems = 1LL << q;
+    j.n_states = n_states;
+    j.init_zero = init_zero ? 1 : 0;
+    std::string err;
+    const size_t jsm = c.jit_smem[pp.jit_index];
+    if (jit_launch(c.jit, pp.jit_index, (unsigned)blocks, threads, jsm, c.stream, j, err) != cudaSuccess)
+      throw GsError(GS_ERR_CUDA, "jit pass launch: " + err);
+    return;
+  }
   if (pp.M == 5) {
     if constexpr (sizeof(R) == 4) launch_pass2_m<R, 5>(c, a, blocks, threads, smem);
   } else {
@@ -1247,6 +1328,7 @@ void gs_destroy(gs_ctx* ctx) {
     if (ctx->c.ev0) cudaEventDestroy(ctx->c.ev0);
     if (ctx->c.ev1) cudaEventDestroy(ctx->c.ev1);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
+    if (ctx->c.jit) gs::jit_release(ctx->c.jit);
   }
   delete ctx;
 }
@@ -1287,6 +1369,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "smem_gather") {
       c.smem_gather = value ? 1 : 0;
+    } else if (k == "jit") {
+      c.use_jit = value ? 1 : 0;
+      if (c.have_prog) gs::jit_program(c);
     } else if (k == "reg_bits") {
       if (value != 4 && value != 5) throw GsError(GS_ERR_ARG, "reg_bits must be 4 or 5");
       c.reg_bits = (int)value;
@@ -1358,7 +1443,9 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
       }
       js += "]}";
     }
-    js += "]}";
+    js += "], \"jit\": \"";
+    for (char ch : c.jit_status) js += (ch == '"' || ch == '\\' || ch == '\n') ? ' ' : ch;
+    js += "\"}";
     if (needed) *needed = (int64_t)js.size() + 1;
     if (buf && cap > 0) {
       const size_t n = std::min<size_t>(js.size(), (size_t)cap - 1);

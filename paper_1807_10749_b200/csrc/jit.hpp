@@ -1,0 +1,46 @@
+// Load-time specialisation of gate passes (NVRTC -> cubin -> driver launch).
+//
+// For every pass of a loaded program the engine emits one straight-line CUDA
+// kernel from the hand-written template in jit.cu: the register stage
+// layout, the shared-memory and HBM element offsets, and every gate
+// coefficient become compile-time constants, so a pass costs its loads,
+// stores and the arithmetic of its gates -- no op decoding, no runtime
+// register-bit dispatch, no per-element address arithmetic.  Cross-gate
+// terms (digit dependent) stay runtime table lookups.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace gs {
+
+// argument block shared by every generated kernel (layout mirrored in the
+// generated source's JArgs)
+struct JArgs {
+  const void* src;
+  void* dst;
+  const int32_t* parent;
+  const unsigned long long* digits;
+  const void* params;   // float4 {rs, t, sn, mode}
+  const int32_t* pxtable;
+  const void* coefs;    // complex coefficient pool (dense cross terms)
+  long long state_elems;
+  long long n_states;
+  int init_zero;
+  int pad;
+};
+
+struct JitModule;
+
+// compile `source` (kernels gsj_0 .. gsj_{n-1}); returns nullptr with `err` set on failure
+JitModule* jit_compile(const std::string& source, int n_kernels, const std::string& tag, std::string& err);
+void jit_release(JitModule* m);
+// launch kernel `idx` of the module
+cudaError_t jit_launch(JitModule* m, int idx, unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                       const JArgs& args, std::string& err);
+bool jit_available(std::string& why);
+
+}  // namespace gs

@@ -59,6 +59,7 @@ struct PassPlan {
   int64_t dev_stage_offset = 0; // into the device stage array
   int64_t goff_offset = 0;      // into the tile-index -> state-offset table
   double store_scale = 1.0;     // power of two applied on store
+  int jit_index = -1;           // kernel gsj_<index> of the program's JIT module
   bool grouped_store = false;   // leaf level, last pass: grouped path-minor store
 };
 
