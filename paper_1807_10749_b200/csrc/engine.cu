@@ -18,6 +18,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/gridsim_b200.h"
@@ -149,7 +150,9 @@ struct Ctx {
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
   int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
   int use_jit = 1;   // specialise passes at load time (NVRTC); interpreter otherwise
-  JitModule* jit = nullptr;
+  std::vector<JitModule*> jit_mods;   // one per compile chunk
+  std::vector<std::pair<int, int>> jit_loc;  // pass jit_index -> (module, kernel)
+  JitModule* jit = nullptr;           // non-null when any module is loaded
   std::string jit_status = "off";
   double jit_seconds = 0;
   std::vector<size_t> jit_smem;
@@ -708,10 +711,10 @@ template <typename T> static void upload(Ctx& c, DevBuf& b, const std::vector<T>
 // Specialise every eligible pass (complex64, 5 register bits) into one NVRTC
 // module.  Failure keeps the interpreter kernels and records why.
 static void jit_program(Ctx& c) {
-  if (c.jit) {
-    jit_release(c.jit);
-    c.jit = nullptr;
-  }
+  for (JitModule* m : c.jit_mods) jit_release(m);
+  c.jit_mods.clear();
+  c.jit_loc.clear();
+  c.jit = nullptr;
   c.jit_smem.clear();
   for (Level& L : c.prog.levels)
     for (int side = 0; side < 2; ++side)
@@ -720,44 +723,84 @@ static void jit_program(Ctx& c) {
     c.jit_status = "off";
     return;
   }
-  std::string src = jitgen::prelude();
-  int n = 0;
+  // one kernel source per eligible pass
+  std::vector<std::string> kernels;
   std::vector<PassPlan*> order;
   for (Level& L : c.prog.levels)
     for (int side = 0; side < 2; ++side)
       for (PassPlan& pp : L.passes[side]) {
         if (pp.M != 5 || pp.stages.empty()) continue;
         size_t smem = 0;
-        src += jitgen::pass_kernel(c, pp, n, smem);
+        const int local = 0;  // renamed per chunk below
+        kernels.push_back(jitgen::pass_kernel(c, pp, local, smem));
         c.jit_smem.push_back(smem);
         order.push_back(&pp);
-        ++n;
       }
+  const int n = (int)kernels.size();
   if (n == 0) {
     c.jit_status = "no eligible passes";
     return;
   }
-  if (const char* dump = std::getenv("GS_JIT_DUMP")) {  // diagnostics: write the generated module
-    if (FILE* f = std::fopen(dump, "w")) {
-      std::fwrite(src.data(), 1, src.size(), f);
-      std::fclose(f);
-    }
+  // chunks compiled concurrently: ~source-size balanced, up to the core count
+  const int hw = std::max(1u, std::thread::hardware_concurrency());
+  const int n_chunks = std::max(1, std::min(n, std::min(hw, 32)));
+  std::vector<std::string> src(n_chunks, jitgen::prelude());
+  std::vector<std::vector<int>> members(n_chunks);
+  std::vector<size_t> load(n_chunks, 0);
+  std::vector<int> by_size(n);
+  for (int i = 0; i < n; ++i) by_size[i] = i;
+  std::sort(by_size.begin(), by_size.end(), [&](int x, int y) { return kernels[x].size() > kernels[y].size(); });
+  for (int i : by_size) {
+    const int ch = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    const int local = (int)members[ch].size();
+    // kernel text was generated as gsj_0: rename to its index inside the chunk
+    std::string k = kernels[i];
+    const size_t at = k.find("gsj_0(");
+    k.replace(at, 6, "gsj_" + std::to_string(local) + "(");
+    src[ch] += k;
+    members[ch].push_back(i);
+    load[ch] += k.size();
+  }
+  if (const char* dump = std::getenv("GS_JIT_DUMP")) {  // diagnostics: write the generated chunks
+    for (int ch = 0; ch < n_chunks; ++ch)
+      if (FILE* f = std::fopen((std::string(dump) + "." + std::to_string(ch) + ".cu").c_str(), "w")) {
+        std::fwrite(src[ch].data(), 1, src[ch].size(), f);
+        std::fclose(f);
+      }
   }
   if (c.host_only) {
-    c.jit_status = "generated " + std::to_string(n) + " kernels (" + std::to_string(src.size()) +
-                   " bytes of source); not compiled on a host-only context";
+    size_t bytes = 0;
+    for (auto& t : src) bytes += t.size();
+    c.jit_status = "generated " + std::to_string(n) + " kernels in " + std::to_string(n_chunks) + " modules (" +
+                   std::to_string(bytes) + " bytes of source); not compiled on a host-only context";
     return;
   }
   const auto t0 = std::chrono::steady_clock::now();
-  std::string err;
-  c.jit = jit_compile(src, n, "gridsim_passes", err);
+  std::vector<JitModule*> mods(n_chunks, nullptr);
+  std::vector<std::string> errs(n_chunks);
+  const int dev = c.device;
+  std::vector<std::thread> pool;
+  for (int ch = 0; ch < n_chunks; ++ch)
+    pool.emplace_back([&, ch] {
+      cudaSetDevice(dev);
+      mods[ch] = jit_compile(src[ch], (int)members[ch].size(), "gridsim_passes_" + std::to_string(ch), errs[ch]);
+    });
+  for (auto& t : pool) t.join();
   c.jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  if (!c.jit) {
-    c.jit_status = "interpreter (jit failed: " + err.substr(0, 300) + ")";
-    return;
-  }
+  for (int ch = 0; ch < n_chunks; ++ch)
+    if (!mods[ch]) {
+      for (JitModule* m : mods) jit_release(m);
+      c.jit_status = "interpreter (jit failed: " + errs[ch].substr(0, 300) + ")";
+      return;
+    }
+  c.jit_mods = mods;
+  c.jit = mods[0];
+  c.jit_loc.assign(n, {0, 0});
+  for (int ch = 0; ch < n_chunks; ++ch)
+    for (size_t k = 0; k < members[ch].size(); ++k) c.jit_loc[members[ch][k]] = {ch, (int)k};
   for (int i = 0; i < n; ++i) order[i]->jit_index = i;
-  c.jit_status = "jit: " + std::to_string(n) + " pass kernels compiled in " + std::to_string(c.jit_seconds) + " s";
+  c.jit_status = "jit: " + std::to_string(n) + " pass kernels, " + std::to_string(n_chunks) +
+                 " modules compiled in " + std::to_string(c.jit_seconds) + " s";
 }
 
 static void upload_program(Ctx& c) {
@@ -970,7 +1013,9 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
     j.init_zero = init_zero ? 1 : 0;
     std::string err;
     const size_t jsm = c.jit_smem[pp.jit_index];
-    if (jit_launch(c.jit, pp.jit_index, (unsigned)blocks, threads, jsm, c.stream, j, err) != cudaSuccess)
+    const auto loc = c.jit_loc[pp.jit_index];
+    if (jit_launch(c.jit_mods[loc.first], loc.second, (unsigned)blocks, threads, jsm, c.stream, j, err) !=
+        cudaSuccess)
       throw GsError(GS_ERR_CUDA, "jit pass launch: " + err);
     return;
   }
@@ -1328,7 +1373,7 @@ void gs_destroy(gs_ctx* ctx) {
     if (ctx->c.ev0) cudaEventDestroy(ctx->c.ev0);
     if (ctx->c.ev1) cudaEventDestroy(ctx->c.ev1);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
-    if (ctx->c.jit) gs::jit_release(ctx->c.jit);
+    for (gs::JitModule* m : ctx->c.jit_mods) gs::jit_release(m);
   }
   delete ctx;
 }

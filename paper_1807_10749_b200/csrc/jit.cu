@@ -4,9 +4,13 @@
 // dependencies.
 #include <cuda.h>
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <nvrtc.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <functional>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -115,10 +119,34 @@ bool jit_available(std::string& why) {
   return true;
 }
 
+// On-disk cubin cache keyed by the generated source (compile time only: a
+// cached cubin is byte-identical to a fresh compile of the same text).
+static std::string cache_path(const std::string& source) {
+  const char* dir = std::getenv("GS_JIT_CACHE");
+  std::string d = dir ? dir : "/tmp/gridsim_b200_jit";
+  if (d.empty() || d == "0") return "";
+  mkdir(d.c_str(), 0755);
+  char name[64];
+  std::snprintf(name, sizeof name, "/%016zx_%zu.cubin", std::hash<std::string>{}(source), source.size());
+  return d + name;
+}
+
+static JitModule* load_cubin(const std::vector<char>& cubin, int n_kernels, std::string& err);
+
 JitModule* jit_compile(const std::string& source, int n_kernels, const std::string& tag, std::string& err) {
   if (!jit_available(err)) return nullptr;
+  const std::string cpath = cache_path(source);
+  if (!cpath.empty()) {
+    if (FILE* f = std::fopen(cpath.c_str(), "rb")) {
+      std::vector<char> cubin;
+      char buf[1 << 16];
+      size_t r;
+      while ((r = std::fread(buf, 1, sizeof buf, f)) > 0) cubin.insert(cubin.end(), buf, buf + r);
+      std::fclose(f);
+      if (JitModule* m = load_cubin(cubin, n_kernels, err)) return m;
+    }
+  }
   NvrtcApi& n = nvrtc();
-  DriverApi& d = driver();
   nvrtcProgram prog;
   nvrtcResult r = n.create(&prog, source.c_str(), (tag + ".cu").c_str(), 0, nullptr, nullptr);
   if (r != NVRTC_SUCCESS) {
@@ -142,6 +170,20 @@ JitModule* jit_compile(const std::string& source, int n_kernels, const std::stri
   std::vector<char> cubin(cs);
   n.cubin(prog, cubin.data());
   n.destroy(&prog);
+  if (!cpath.empty()) {
+    const std::string tmp = cpath + ".tmp" + std::to_string(getpid());
+    if (FILE* f = std::fopen(tmp.c_str(), "wb")) {
+      const bool ok = std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+      std::fclose(f);
+      if (ok) std::rename(tmp.c_str(), cpath.c_str());
+      else std::remove(tmp.c_str());
+    }
+  }
+  return load_cubin(cubin, n_kernels, err);
+}
+
+static JitModule* load_cubin(const std::vector<char>& cubin, int n_kernels, std::string& err) {
+  DriverApi& d = driver();
   auto m = std::make_unique<JitModule>();
   CUresult cr = d.load(&m->mod, cubin.data());
   if (cr != CUDA_SUCCESS) {
