@@ -125,6 +125,13 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed);
  * Host arrays; validated against the loaded program's block sizes and uploaded. */
 int gs_set_requests(gs_ctx* ctx, int64_t n_req, const int64_t* idx_a, const int64_t* idx_b);
 
+/* Same, from global basis indices (qubit 0 = most significant bit): the split
+ * into block-local indices runs on the device.  block_a / block_b list each
+ * block's global qubits in ascending order (the cut).  GS_ERR_INDEX when an
+ * index is outside [0, 2^n_qubits). */
+int gs_set_requests_global(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32_t n_qubits,
+                           const int32_t* block_a, const int32_t* block_b);
+
 /* Sum the contributions of the leaves {(p, b) : p in prefixes, branch_lo <= b < branch_hi}
  * where path id = p * branch_space + b and the first x_p cross digits are the
  * prefix (SimPlan, pathsum.py:246-274).  `prefixes` need not be sorted; each

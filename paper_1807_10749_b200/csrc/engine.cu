@@ -158,7 +158,7 @@ struct Ctx {
   std::vector<size_t> jit_smem;
   // requests
   int64_t n_req = -1;
-  DevBuf d_ia, d_ib, d_acc, d_partial;
+  DevBuf d_ia, d_ib, d_acc, d_partial, d_gidx;
   // tree buffers
   std::vector<DevBuf> lvl_a, lvl_b, lvl_parent, lvl_digit;
   std::vector<PinnedBuf> lvl_stage;
@@ -1497,6 +1497,61 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
       std::memcpy(buf, js.data(), n);
       buf[n] = 0;
     }
+  });
+}
+
+int gs_set_requests_global(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32_t n_qubits,
+                           const int32_t* block_a, const int32_t* block_b) {
+  if (!ctx) return GS_ERR_ARG;
+  GS_GUARD(ctx, {
+    Ctx& c = ctx->c;
+    if (!c.have_prog) throw GsError(GS_ERR_STATE, "no program loaded");
+    if (n_req < 0 || (n_req > 0 && !idx) || !block_a || !block_b) throw GsError(GS_ERR_ARG, "bad request arrays");
+    const int qs[2] = {c.prog.q[0], c.prog.q[1]};
+    if (qs[0] + qs[1] != n_qubits || n_qubits > 62) throw GsError(GS_ERR_ARG, "cut does not match the program");
+    // runs of consecutive qubits; qubit q owns global bit n-1-q, local j owns bit q_blk-1-j
+    gs::SplitRuns runs{};
+    runs.qa = qs[0];
+    std::vector<char> seen(n_qubits, 0);
+    for (int b = 0; b < 2; ++b) {
+      const int32_t* blk = b ? block_b : block_a;
+      int j = 0;
+      while (j < qs[b]) {
+        int k = j;
+        while (k + 1 < qs[b] && blk[k + 1] == blk[k] + 1) ++k;
+        for (int t = j; t <= k; ++t) {
+          if (blk[t] < 0 || blk[t] >= n_qubits || seen[blk[t]]) throw GsError(GS_ERR_ARG, "bad cut blocks");
+          seen[blk[t]] = 1;
+        }
+        if (runs.n[b] >= 32) throw GsError(GS_ERR_ARG, "cut has too many bit runs");
+        runs.src[b][runs.n[b]] = n_qubits - 1 - blk[k];
+        runs.width[b][runs.n[b]] = k - j + 1;
+        runs.dst[b][runs.n[b]] = qs[b] - 1 - k;
+        ++runs.n[b];
+        j = k + 1;
+      }
+    }
+    const int64_t lim = 1LL << n_qubits;
+    for (int64_t i = 0; i < n_req; ++i)
+      if (idx[i] < 0 || idx[i] >= lim) throw GsError(GS_ERR_INDEX, "request index outside the state space");
+    c.n_req = -1;
+    if (!c.host_only) {
+      CK(cudaSetDevice(c.device));
+      c.d_gidx.ensure(std::max<size_t>(n_req * 8, 16));
+      c.d_ia.ensure(std::max<size_t>(n_req * 4, 16));
+      c.d_ib.ensure(std::max<size_t>(n_req * 4, 16));
+      const bool pk = qs[0] + qs[1] <= 31;
+      if (pk) c.d_packed.ensure(std::max<size_t>(n_req * 4, 16));
+      c.d_acc.ensure(std::max<size_t>(n_req * sizeof(double2), 16));
+      if (n_req > 0) {
+        CK(cudaMemcpyAsync(c.d_gidx.p, idx, n_req * 8, cudaMemcpyHostToDevice, c.stream));
+        gs::split_kernel<<<(unsigned)((n_req + 255) / 256), 256, 0, c.stream>>>(
+            reinterpret_cast<const long long*>(c.d_gidx.p), n_req, runs, reinterpret_cast<int32_t*>(c.d_ia.p),
+            reinterpret_cast<int32_t*>(c.d_ib.p), pk ? reinterpret_cast<uint32_t*>(c.d_packed.p) : nullptr);
+        CK(cudaGetLastError());
+      }
+    }
+    c.n_req = n_req;
   });
 }
 

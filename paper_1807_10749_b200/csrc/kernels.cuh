@@ -360,4 +360,33 @@ gather_grouped_kernel(const void* A, const void* B, long long a_elems, long long
   partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
 }
 
+
+// ---------------------------------------------------------------------------
+// Request split on the device (split_requests, pathsum.py:122-140): global
+// index -> block-local indices, one shift+mask per run of consecutive qubits.
+
+struct SplitRuns {
+  int n[2];
+  int src[2][32];   // global bit of the run's lowest bit
+  int width[2][32];
+  int dst[2][32];   // local bit of the run's lowest bit
+  int qa;
+};
+
+static __global__ void __launch_bounds__(256)
+split_kernel(const long long* idx, long long n_req, const SplitRuns r, int32_t* ia, int32_t* ib,
+             uint32_t* packed) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req) return;
+  const unsigned long long x = (unsigned long long)idx[i];
+  unsigned out[2] = {0u, 0u};
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+    for (int k = 0; k < r.n[b]; ++k)
+      out[b] |= (unsigned)((x >> r.src[b][k]) & ((1ull << r.width[b][k]) - 1)) << r.dst[b][k];
+  ia[i] = (int32_t)out[0];
+  ib[i] = (int32_t)out[1];
+  if (packed) packed[i] = out[0] | (out[1] << r.qa);
+}
+
 }  // namespace gs

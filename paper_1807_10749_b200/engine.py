@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "gs_set_requests",
     "gs_run",
     "gs_describe",
+    "gs_set_requests_global",
 )
 
 
@@ -92,6 +93,7 @@ def _load():
         ctypes.c_int64, _F64P,
     ]
     lib.gs_set_requests.argtypes = [_P, ctypes.c_int64, _I64P, _I64P]
+    lib.gs_set_requests_global.argtypes = [_P, ctypes.c_int64, _I64P, ctypes.c_int32, _I32P, _I32P]
     lib.gs_describe.argtypes = [_P, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
     lib.gs_run.argtypes = [
         _P, ctypes.c_int32, ctypes.c_int64, _I64P, ctypes.c_int64, ctypes.c_int64,
@@ -226,6 +228,18 @@ class Engine:
         buf = ctypes.create_string_buffer(int(need.value))
         self._check(LIB.gs_describe(self._h, buf, need.value, ctypes.byref(need)))
         return json.loads(buf.value.decode())
+
+    def set_requests_global(self, indices, n_qubits: int, block_a, block_b):
+        """Upload global indices; the device splits them for the loaded cut."""
+        idx = np.ascontiguousarray(indices, dtype=np.int64).ravel()
+        pidx = idx if idx.size else np.zeros(1, dtype=np.int64)
+        ba = np.ascontiguousarray(block_a, dtype=np.int32)
+        bb = np.ascontiguousarray(block_b, dtype=np.int32)
+        self._check(LIB.gs_set_requests_global(
+            self._h, idx.size, _ptr(pidx, ctypes.c_int64), int(n_qubits),
+            _ptr(ba, ctypes.c_int32), _ptr(bb, ctypes.c_int32)))
+        self._requests = None
+        self.n_req = int(idx.size)
 
     def set_requests(self, idx_a: np.ndarray, idx_b: np.ndarray, key=None):
         if key is not None and self._requests is not None and self._requests == key:

@@ -30,7 +30,7 @@ from .amplitudes import AmplitudeBatch
 from .circuit import Circuit
 from .engine import ENGINES
 from .lowering import lowered
-from .plan import SimPlan, path_digits, split_requests
+from .plan import SimPlan, path_digits
 
 ENGINE_NAMES = ("b200", "batched", "perjob")
 
@@ -39,11 +39,11 @@ def _engine_for(circuit: Circuit, plan: SimPlan, requests, device: int, dtype):
     prog = lowered(circuit, plan.cut)
     if prog.radices != tuple(int(r) for r in plan.radices):
         raise ValueError("plan radices do not match the circuit's cross gates under plan.cut")
-    idx = np.asarray(requests, dtype=np.int64)
-    idx_a, idx_b = split_requests(circuit.n_qubits, plan.cut.block_a, plan.cut.block_b, idx)
+    idx = np.asarray(requests, dtype=np.int64).ravel()
     eng = ENGINES.get(device, dtype)
     eng.load_program(prog)
-    eng.set_requests(idx_a, idx_b)
+    # split_requests (pathsum.py:122-140) runs on the device; IndexError as in the reference
+    eng.set_requests_global(idx, circuit.n_qubits, plan.cut.block_a, plan.cut.block_b)
     return eng, idx
 
 

@@ -116,3 +116,19 @@ def test_scheduler_covers_all_ops(tile_bits):
     st = eng.run(plan.x_p, pre[:64], 0, plan.branch_space).stats
     assert st["n_paths"] == 64 * plan.branch_space
     assert st["n_pass_launches"] >= 2 * st["n_levels"]
+
+
+def test_set_requests_global_validation():
+    circ, plan, req, _ = configs.build("cfg1", n_req=8)
+    eng = host_engine()
+    eng.load_program(lowered(circ, plan.cut))
+    eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+    assert eng.n_req == req.size
+    with pytest.raises(IndexError):
+        eng.set_requests_global(np.array([1 << 16]), 16, plan.cut.block_a, plan.cut.block_b)
+    with pytest.raises(IndexError):
+        eng.set_requests_global(np.array([-1]), 16, plan.cut.block_a, plan.cut.block_b)
+    with pytest.raises(ValueError):
+        eng.set_requests_global(req, 15, plan.cut.block_a, plan.cut.block_b)
+    with pytest.raises(ValueError):
+        eng.set_requests_global(req, 16, plan.cut.block_a, plan.cut.block_a)
