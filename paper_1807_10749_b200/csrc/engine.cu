@@ -526,8 +526,11 @@ static void schedule_program(Ctx& c) {
   // from HBM (half-states too large for the shared-memory gather).
   {
     const size_t pair_bytes = (((size_t)1 << p.q[0]) + ((size_t)1 << p.q[1])) * c.esize();
+    // grouping costs the leaf level group_log tile bits (possibly an extra pass);
+    // it pays while a leaf's random-sector gather traffic (~40 B per request) is
+    // comparable to its pass traffic, i.e. up to ~2^24-amplitude halves
     c.grouped_leaf = c.kernel_version == 2 && c.grouped_enabled && 2 * pair_bytes > 200 * 1024 &&
-                     std::min(p.q[0], p.q[1]) >= 12;
+                     std::min(p.q[0], p.q[1]) >= 12 && std::max(p.q[0], p.q[1]) <= 24;
   }
   const int D = (int)p.levels.size() - 1;
   for (size_t l = 0; l < p.levels.size(); ++l) {
