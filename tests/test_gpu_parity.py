@@ -133,3 +133,34 @@ def test_errors(ps):
     assert empty.amps.shape == (0,)
     none = ps.run_batched(circ, plan, req, prefixes=np.array([], dtype=np.int64))
     assert np.all(none.amps == 0)
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg5f"])
+def test_cfg5_full_size_c64_matches_c128(ps, name):
+    """28|28 halves (2 GiB each): the complex64 specialised kernels agree with the
+    complex128 kernels on the same leading path and branch set, and summing a
+    prefix's branches equals the sum of its single paths (linearity)."""
+    circ, plan, _, pre = configs.build(name, n_req=4)
+    from paper_1807_10749_b200 import challenge_indices
+
+    req = challenge_indices(circ.n_qubits, 2048, 12345)
+    pid = int(pre[0]) * plan.branch_space
+    p64 = ps.run_path(circ, plan, pid, req).amps
+    p128 = ps.run_path(circ, plan, pid, req, dtype="c128").amps
+    assert np.linalg.norm(p128) > 0
+    assert rel_l2(p64, p128) <= C64_TOL
+    nb = min(plan.branch_space, 4)
+    singles = sum(ps.run_path(circ, plan, pid + b, req).amps for b in range(nb))
+    if nb == plan.branch_space:
+        tree = ps.run_prefix_tree(circ, plan, int(pre[0]), req).amps
+        assert rel_l2(tree, singles) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg5f"])
+def test_cfg5_reference_paths(ps, name):
+    """Per-path parity with the reference at 28|28 (tests/golden/amps/<name>.npz,
+    produced by the reference's run_path in the build container)."""
+    g = load_amps(name)
+    circ, plan, _, _ = configs.build(name, n_req=4)
+    for pid, want in zip(g["path_ids"], g["path_amps"]):
+        assert rel_l2(ps.run_path(circ, plan, int(pid), g["requests"]).amps, want) <= C64_TOL
