@@ -1603,12 +1603,12 @@ int gs_run(gs_ctx* ctx, int32_t x_p, int64_t n_prefix, const int64_t* prefixes, 
     c.x_p = x_p;
     c.S_p.assign(x_p + 1, 1);
     for (int k = x_p - 1; k >= 0; --k) {
-      if (c.S_p[k + 1] > (INT64_MAX / 2) / p.radix[k]) throw GsError(GS_ERR_ARG, "prefix space exceeds 2^62");
+      if (c.S_p[k + 1] > (1LL << 62) / p.radix[k]) throw GsError(GS_ERR_ARG, "prefix space exceeds 2^62");
       c.S_p[k] = c.S_p[k + 1] * p.radix[k];
     }
     c.S_b.assign(x + 1, 1);
     for (int k = x - 1; k >= x_p; --k) {
-      if (c.S_b[k + 1] > (INT64_MAX / 2) / p.radix[k]) throw GsError(GS_ERR_ARG, "branch space exceeds 2^62");
+      if (c.S_b[k + 1] > (1LL << 62) / p.radix[k]) throw GsError(GS_ERR_ARG, "branch space exceeds 2^62");
       c.S_b[k] = c.S_b[k + 1] * p.radix[k];
     }
     const int64_t prefix_space = c.S_p[0], branch_space = c.S_b[x_p];
