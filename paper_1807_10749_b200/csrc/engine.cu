@@ -9,6 +9,8 @@
 // accumulator on the device.
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -145,6 +147,10 @@ struct Ctx {
   int smem_gather = 1;
   int grouped_enabled = 1;
   bool grouped_leaf = false;
+  int fuse_gather = 1;        // option: gather inside the last B-side leaf pass (JIT only)
+  bool fused_active = false;  // the fused leaf pass is compiled for the loaded program
+  bool bucket_valid = false;  // request buckets match the loaded requests
+  DevBuf d_bcount, d_bstart, d_breq, d_btl, d_cubtmp;
   int group_log = 3;  // leaves per group = 2^group_log (64-byte request reads in c64)
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
@@ -538,7 +544,11 @@ static void schedule_program(Ctx& c) {
     for (int side = 0; side < 2; ++side) {
       const int kcap = ((int)l == D && c.grouped_leaf) ? c.kmax() - c.group_log : c.kmax();
       L.passes[side] = schedule_passes(L.ops[side], p.q[side], kcap, c.low_bits, true);
-      if ((int)l == D && c.grouped_leaf) L.passes[side].back().grouped_store = true;
+      if ((int)l == D && c.grouped_leaf) {
+        L.passes[side].back().grouped_store = true;
+        if (side == 1 && c.fuse_gather && c.group_log == 3 && c.precision == GS_C64)
+          L.passes[side].back().fused_gather = true;
+      }
       for (PassPlan& pp : L.passes[side]) {
         pp.dev_op_offset = (int64_t)c.host_devops.size();
         std::vector<int> tpos(p.q[side], -1);
@@ -714,6 +724,8 @@ template <typename T> static void upload(Ctx& c, DevBuf& b, const std::vector<T>
 // Specialise every eligible pass (complex64, 5 register bits) into one NVRTC
 // module.  Failure keeps the interpreter kernels and records why.
 static void jit_program(Ctx& c) {
+  c.fused_active = false;
+  c.bucket_valid = false;
   for (JitModule* m : c.jit_mods) jit_release(m);
   c.jit_mods.clear();
   c.jit_loc.clear();
@@ -735,7 +747,7 @@ static void jit_program(Ctx& c) {
         if (pp.M != 5 || pp.stages.empty()) continue;
         size_t smem = 0;
         const int local = 0;  // renamed per chunk below
-        kernels.push_back(jitgen::pass_kernel(c, pp, local, smem));
+        kernels.push_back(jitgen::pass_kernel(c, pp, local, smem, pp.fused_gather));
         c.jit_smem.push_back(smem);
         order.push_back(&pp);
       }
@@ -802,6 +814,7 @@ static void jit_program(Ctx& c) {
   for (int ch = 0; ch < n_chunks; ++ch)
     for (size_t k = 0; k < members[ch].size(); ++k) c.jit_loc[members[ch][k]] = {ch, (int)k};
   for (int i = 0; i < n; ++i) order[i]->jit_index = i;
+  for (PassPlan* pp : order) c.fused_active |= pp->fused_gather;
   c.jit_status = "jit: " + std::to_string(n) + " pass kernels, " + std::to_string(n_chunks) +
                  " modules compiled in " + std::to_string(c.jit_seconds) + " s";
 }
@@ -1014,6 +1027,17 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
     j.state_elems = 1LL << q;
     j.n_states = n_states;
     j.init_zero = init_zero ? 1 : 0;
+    if (pp.fused_gather) {
+      j.aleaf = c.leaf_out[0].p;
+      j.ia = reinterpret_cast<const int32_t*>(c.d_ia.p);
+      j.weights = reinterpret_cast<const double*>(c.d_weights.p);
+      j.bstart = reinterpret_cast<const int32_t*>(c.d_bstart.p);
+      j.breq = reinterpret_cast<const int32_t*>(c.d_breq.p);
+      j.btl = reinterpret_cast<const int32_t*>(c.d_btl.p);
+      j.partial = c.d_partial.p;
+      j.n_req = c.n_req;
+      j.a_elems = 1LL << c.prog.q[0];
+    }
     std::string err;
     const size_t jsm = c.jit_smem[pp.jit_index];
     const auto loc = c.jit_loc[pp.jit_index];
@@ -1079,22 +1103,45 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
     c.st.pass_bytes_min += 2.0 * (double)n * (double)(1LL << c.prog.q[side]) * (double)c.esize();
 }
 
-template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64_t n) {
-  // leaf multiplicity: duplicate prefixes / branch ranges collapsed into one node
-  int64_t w_total = 0;
-  for (int64_t j = 0; j < n; ++j) w_total += (nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0);
-  c.st.n_paths += w_total;
-  if (c.host_only || c.n_req == 0) return;
+// leaf multiplicities (duplicate prefixes / branch ranges collapsed into one node)
+static void upload_weights(Ctx& c, const Node* nodes, int64_t n) {
+  if (c.host_only || n == 0) return;
   c.weights_stage.ensure(n * sizeof(double));
   cudaEventSynchronize(c.weights_event);
   double* w = reinterpret_cast<double*>(c.weights_stage.p);
   for (int64_t j = 0; j < n; ++j) w[j] = (double)((nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0));
-  Timer t(c, &c.st.ms_gather);
   c.d_weights.ensure(std::max<size_t>(n * sizeof(double), 16));
   CK(cudaMemcpyAsync(c.d_weights.p, w, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
   c.st.h2d_bytes += 8.0 * n;
   CK(cudaEventRecord(c.weights_event, c.stream));
+  if (c.fused_active) {  // partials of the fused leaf gather, one row per group of 8 leaves
+    const size_t groups = (size_t)((n + 7) / 8);
+    c.d_partial.ensure(std::max<size_t>(groups * (size_t)std::max<int64_t>(c.n_req, 1) * sizeof(double2), 16));
+  }
+}
+
+template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64_t n) {
+  int64_t w_total = 0;
+  for (int64_t j = 0; j < n; ++j) w_total += (nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0);
+  c.st.n_paths += w_total;
+  if (c.host_only || c.n_req == 0) return;
+  Timer t(c, &c.st.ms_gather);
   const int64_t nreq = c.n_req;
+  if (c.fused_active) {  // partials were written by the fused leaf pass
+    const int threads = 256;
+    const int64_t xblocks = (nreq + threads - 1) / threads;
+    const int64_t groups = (n + 7) / 8;
+    const double ar = c.kfinal[0][0], ai = c.kfinal[0][1], br = c.kfinal[1][0], bi = c.kfinal[1][1];
+    const double2 kf = make_double2(ar * br - ai * bi, ar * bi + ai * br);
+    reduce_kernel<<<(unsigned)xblocks, threads, 0, c.stream>>>(reinterpret_cast<const double2*>(c.d_partial.p),
+                                                                (int)groups, nreq, kf,
+                                                                reinterpret_cast<double2*>(c.d_acc.p));
+    launch_check("reduce_kernel", xblocks, threads, 0);
+    c.st.n_gather_launches += 1;
+    c.st.n_launches += 1;
+    c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
+    return;
+  }
   const int threads = 256;
   const int64_t xblocks = (nreq + threads - 1) / threads;
   // enough leaf groups to fill the GPU, bounded by the partial buffer
@@ -1193,6 +1240,7 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
       c.st.h2d_bytes += 12.0 * n;
       CK(cudaEventRecord(c.lvl_event[l + 1], c.stream));
     }
+    if (l + 1 == D) upload_weights(c, chunk, n);  // the fused leaf pass reads them
     run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
                         at(c.lvl_b, l + 1), reinterpret_cast<const int32_t*>(at(c.lvl_parent, l + 1)),
                         reinterpret_cast<const uint64_t*>(at(c.lvl_digit, l + 1)), false);
@@ -1243,6 +1291,10 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
   }
   c.cap.assign(D + 1, 1);
   for (int l = 0; l <= D; ++l) c.cap[l] = (int64_t)std::max(1.0, std::min(bound[l], lo));
+  if (c.fused_active && c.n_req > 0) {  // fused leaf gather: one partial row per 8 leaves
+    const int64_t max_groups = std::max<int64_t>(1, (2LL << 30) / (16 * c.n_req));
+    c.cap[D] = std::min<int64_t>(c.cap[D], 8 * max_groups);
+  }
   if (c.host_only) return;
   c.lvl_a.resize(D + 1);
   c.lvl_b.resize(D + 1);
@@ -1274,6 +1326,41 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
   }
 }
 
+// Bucket the requests by the tile of the fused leaf pass (B side, last pass):
+// counting sort on the device (histogram, CUB exclusive scan, scatter).
+static void build_buckets(Ctx& c) {
+  const int D = (int)c.prog.levels.size() - 1;
+  const PassPlan& pp = c.prog.levels[D].passes[1].back();
+  BucketMap m{};
+  m.n_g = (int)pp.gbits.size();
+  m.n_l = pp.k;
+  for (int j = 0; j < m.n_g; ++j) m.gbits[j] = pp.gbits[j];
+  for (int j = 0; j < m.n_l; ++j) m.lbits[j] = pp.lbits[j];
+  const int tiles = 1 << m.n_g;
+  const int64_t n = c.n_req;
+  c.d_bcount.ensure((size_t)(tiles + 1) * 4);
+  c.d_bstart.ensure((size_t)(tiles + 1) * 4);
+  c.d_breq.ensure(std::max<size_t>((size_t)n * 4, 16));
+  c.d_btl.ensure(std::max<size_t>((size_t)n * 4, 16));
+  int32_t* cnt = reinterpret_cast<int32_t*>(c.d_bcount.p);
+  int32_t* start = reinterpret_cast<int32_t*>(c.d_bstart.p);
+  CK(cudaMemsetAsync(cnt, 0, (size_t)(tiles + 1) * 4, c.stream));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, (n + 255) / 256);
+  if (n > 0)
+    bucket_count_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const int32_t*>(c.d_ib.p), n, m, cnt);
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, tiles + 1, c.stream));
+  c.d_cubtmp.ensure(std::max<size_t>(tmp, 16));
+  CK(cub::DeviceScan::ExclusiveSum(c.d_cubtmp.p, tmp, cnt, start, tiles + 1, c.stream));
+  CK(cudaMemcpyAsync(cnt, start, (size_t)(tiles + 1) * 4, cudaMemcpyDeviceToDevice, c.stream));
+  if (n > 0)
+    bucket_fill_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const int32_t*>(c.d_ib.p), n, m, cnt,
+                                                     reinterpret_cast<int32_t*>(c.d_breq.p),
+                                                     reinterpret_cast<int32_t*>(c.d_btl.p));
+  CK(cudaGetLastError());
+  c.bucket_valid = true;
+}
+
 template <typename R>
 static void run_tree(Ctx& c) {
   const Program& p = c.prog;
@@ -1281,6 +1368,9 @@ static void run_tree(Ctx& c) {
   int64_t n_leaves_bound = (int64_t)c.prefixes.size() * (c.branch_hi - c.branch_lo);
   plan_buffers(c, std::max<int64_t>(1, n_leaves_bound));
   c.st.n_levels = D + 1;
+  if (c.fused_active && !c.host_only && !c.bucket_valid && c.n_req > 0) build_buckets(c);
+  const Node root0{0, (int64_t)c.prefixes.size(), 0, 0, c.branch_lo, c.branch_hi, 0, 0};
+  if (D == 0) upload_weights(c, &root0, 1);  // the root is the leaf
   // root: |0...0> through the root segment
   run_level_passes<R>(c, 0, 1, nullptr, nullptr, c.lvl_a.empty() ? nullptr : c.lvl_a[0].p,
                       c.lvl_b.empty() ? nullptr : c.lvl_b[0].p, nullptr, nullptr, true);
@@ -1411,6 +1501,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "group_log") {
       if (value != 2 && value != 3) throw GsError(GS_ERR_ARG, "group_log must be 2 or 3");
       c.group_log = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "fuse_gather") {
+      c.fuse_gather = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "grouped_leaf") {
       c.grouped_enabled = value ? 1 : 0;
@@ -1555,6 +1648,7 @@ int gs_set_requests_global(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32
       }
     }
     c.n_req = n_req;
+    c.bucket_valid = false;
   });
 }
 
@@ -1584,6 +1678,7 @@ int gs_set_requests(gs_ctx* ctx, int64_t n_req, const int64_t* ia, const int64_t
       c.d_acc.ensure(std::max<size_t>(n_req * sizeof(double2), 16));
     }
     c.n_req = n_req;
+    c.bucket_valid = false;
   });
 }
 

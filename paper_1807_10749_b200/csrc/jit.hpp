@@ -31,6 +31,16 @@ struct JArgs {
   long long n_states;
   int init_zero;
   int pad;
+  // fused leaf gather (last B-side leaf pass): requests bucketed by B tile
+  const void* aleaf;          // grouped A leaf states [leaf/8][x][8]
+  const int32_t* ia;          // A-local index per request
+  const double* weights;      // leaf multiplicities
+  const int32_t* bstart;      // bucket offsets per B tile (tiles + 1)
+  const int32_t* breq;        // request index per bucket slot
+  const int32_t* btl;         // tile-local B index per bucket slot
+  void* partial;              // double2 [leaf group][n_req]
+  long long n_req;
+  long long a_elems;
 };
 
 struct JitModule;

@@ -389,4 +389,42 @@ split_kernel(const long long* idx, long long n_req, const SplitRuns r, int32_t* 
   if (packed) packed[i] = out[0] | (out[1] << r.qa);
 }
 
+
+// ---------------------------------------------------------------------------
+// Requests bucketed by the tile of the last B-side leaf pass (fused gather):
+// tile id = the B-local bits outside the tile, tile-local index = the bits
+// inside it (both pext-style over the pass's bit lists).
+
+struct BucketMap {
+  int n_g, n_l;
+  int gbits[32];
+  int lbits[16];
+};
+
+static __device__ __forceinline__ void bucket_of(const BucketMap& m, unsigned ib, unsigned& tile, unsigned& tl) {
+  tile = 0;
+  tl = 0;
+  for (int j = 0; j < m.n_g; ++j) tile |= ((ib >> m.gbits[j]) & 1u) << j;
+  for (int j = 0; j < m.n_l; ++j) tl |= ((ib >> m.lbits[j]) & 1u) << j;
+}
+
+static __global__ void bucket_count_kernel(const int32_t* ib, long long n, const BucketMap m, int32_t* count) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned t, l;
+  bucket_of(m, (unsigned)ib[i], t, l);
+  atomicAdd(count + t, 1);
+}
+
+static __global__ void bucket_fill_kernel(const int32_t* ib, long long n, const BucketMap m, int32_t* cursor,
+                                          int32_t* breq, int32_t* btl) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned t, l;
+  bucket_of(m, (unsigned)ib[i], t, l);
+  const int pos = atomicAdd(cursor + t, 1);
+  breq[pos] = (int32_t)i;
+  btl[pos] = (int32_t)l;
+}
+
 }  // namespace gs

@@ -61,6 +61,7 @@ struct PassPlan {
   double store_scale = 1.0;     // power of two applied on store
   int jit_index = -1;           // kernel gsj_<index> of the program's JIT module
   bool grouped_store = false;   // leaf level, last pass: grouped path-minor store
+  bool fused_gather = false;    // leaf level, last B pass: gather instead of a B store (JIT)
 };
 
 struct Level {
