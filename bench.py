@@ -270,6 +270,9 @@ def main():
     eng.set_option("profile", 1)
     prof = step(args.warmup % n_steps_total)
     eng.set_option("profile", 0)
+    # steps are queued back to back: the host enumerates step s+1's path tree
+    # while the device runs step s (stream order; results land in `out`)
+    eng.set_option("async_run", 1)
 
     torch.cuda.synchronize()
     if world > 1:
@@ -284,6 +287,7 @@ def main():
         step(args.warmup + s, stats)
     e1.record(stream)
     torch.cuda.synchronize()
+    eng.set_option("async_run", 0)
     clk.mark(False)
     clk.stop()
     ms = e0.elapsed_time(e1)

@@ -24,7 +24,8 @@
  *  - The caller owns every host buffer; the library copies in/out and keeps no
  *    host pointer after a call returns.
  *  - One call in flight per context.  Calls are synchronous: when gs_run
- *    returns, the result is in the output buffer.
+ *    returns, the result is in the output buffer (unless option
+ *    "async_run" is set and the output is device memory).
  *  - Contexts are per process and per device; create them after any fork()
  *    (the reference orchestrator forks workers, orchestrator.py:237).
  */
@@ -90,12 +91,23 @@ int gs_create(int device, int precision, gs_ctx** out);
 void gs_destroy(gs_ctx* ctx);
 const char* gs_last_error(const gs_ctx* ctx);
 
-/* Run on a caller-provided cudaStream_t (NULL: the context's own stream). */
+/* Run on a caller-provided cudaStream_t (NULL: the context's own stream).
+ * Waits for the work already queued on the previous stream. */
 int gs_set_stream(gs_ctx* ctx, void* cuda_stream);
 
-/* Integer options: "mem_budget_mb" (device memory for path-tree buffers),
- * "profile" (0/1), "tile_bits" (shared-memory tile width, 8..13),
- * "merge_levels" (0/1: cost-model level merging), "max_chunk" (nodes/launch). */
+/* Integer options (unknown key or out-of-range value: GS_ERR_ARG):
+ *   "mem_budget_mb"  device memory for path-tree buffers (0 = 80% of free)
+ *   "profile"        0/1: events around every level (fills ms_pass/ms_gather)
+ *   "tile_bits"      0 (auto) or 4..14: shared-memory tile width of a pass
+ *   "max_chunk"      nodes per level launch, upper bound
+ *   "hoist"          0/1: move digit-independent gates above branch points
+ *   "smem_gather", "grouped_leaf", "group_log", "fuse_gather": leaf gather
+ *                    variants
+ *   "jit"            0/1: load-time specialised pass kernels (NVRTC)
+ *   "reg_bits", "pass_kernel": interpreter kernel variants
+ *   "async_run"      0/1: with a device output and no host output, gs_run
+ *                    returns once the step is queued on the stream (stats
+ *                    ms_total = -1); the caller orders on that stream. */
 int gs_set_option(gs_ctx* ctx, const char* key, int64_t value);
 
 /* Load the lowered op stream of one circuit under one cut.

@@ -21,6 +21,7 @@
 #include <numeric>
 #include <string>
 #include <thread>
+#include <deque>
 #include <vector>
 
 #include "../../include/gridsim_b200.h"
@@ -88,6 +89,76 @@ struct PinnedBuf {
   }
 };
 
+// Host->device staging ring for per-chunk node tables (digits, parents, leaf
+// weights).  Every region gets an event after its copy; the host waits only
+// when it is about to overwrite a region whose copy may still be pending, so
+// the launch queue of a step is never drained by staging.  All copies and
+// kernels run on one stream, so the device-side region is free for reuse by
+// stream order.
+struct Ring {
+  PinnedBuf host;
+  DevBuf dev;
+  size_t size = 0, head = 0;
+  struct Region {
+    size_t beg, end;
+    cudaEvent_t ev;
+  };
+  std::deque<Region> inflight;
+  std::vector<cudaEvent_t> pool;
+  ~Ring() {
+    for (auto& r : inflight) cudaEventDestroy(r.ev);
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+  void drain() {
+    for (auto& r : inflight) {
+      cudaEventSynchronize(r.ev);
+      pool.push_back(r.ev);
+    }
+    inflight.clear();
+  }
+  // grow to at least n bytes (waits for pending copies before reallocating)
+  void reserve(size_t n, cudaStream_t s) {
+    if (n <= size) return;
+    drain();
+    CK(cudaStreamSynchronize(s));
+    host.ensure(n);
+    dev.ensure(n);
+    size = n;
+    head = 0;
+  }
+  // region of `bytes` (256-aligned) whose host side is free to write
+  size_t alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    if (bytes > size) throw GsError(GS_ERR_STATE, "staging ring too small");
+    if (head + bytes > size) head = 0;
+    const size_t beg = head, end = head + bytes;
+    int last = -1;
+    for (int i = 0; i < (int)inflight.size(); ++i)
+      if (inflight[i].beg < end && beg < inflight[i].end) last = i;
+    if (last >= 0) {
+      cudaEventSynchronize(inflight[last].ev);
+      for (int i = 0; i <= last; ++i) {
+        pool.push_back(inflight.front().ev);
+        inflight.pop_front();
+      }
+    }
+    head = end;
+    return beg;
+  }
+  // copy [off, off + bytes) to the device and mark it in flight
+  void commit(size_t off, size_t bytes, cudaStream_t s) {
+    CK(cudaMemcpyAsync(static_cast<char*>(dev.p) + off, static_cast<char*>(host.p) + off, bytes,
+                       cudaMemcpyHostToDevice, s));
+    cudaEvent_t e;
+    if (pool.empty()) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    else e = pool.back(), pool.pop_back();
+    CK(cudaEventRecord(e, s));
+    inflight.push_back({off, off + ((bytes + 255) & ~(size_t)255), e});
+  }
+  char* h(size_t off) { return static_cast<char*>(host.p) + off; }
+  char* d(size_t off) { return static_cast<char*>(dev.p) + off; }
+};
+
 // Node of the path tree.  Leaves are (prefix index i, branch b); a node at
 // level l with digit end e covers the prefixes i0..i1-1 (all sharing digits
 // [0, min(e, x_p))) and the branch ids b0..b1-1 (all sharing digits
@@ -147,10 +218,11 @@ struct Ctx {
   int smem_gather = 1;
   int grouped_enabled = 1;
   bool grouped_leaf = false;
-  int fuse_gather = 1;        // option: gather inside the last B-side leaf pass (JIT only)
+  int fuse_gather = 0;        // option: gather inside the last B-side leaf pass (JIT only; slower: the
+                              // epilogue is latency-bound and stalls the pass, profiles/r01_notes.md)
   bool fused_active = false;  // the fused leaf pass is compiled for the loaded program
   bool bucket_valid = false;  // request buckets match the loaded requests
-  DevBuf d_bcount, d_bstart, d_breq, d_btl, d_cubtmp;
+  DevBuf d_bcount, d_bstart, d_breq, d_btl, d_bia, d_cubtmp;
   int group_log = 3;  // leaves per group = 2^group_log (64-byte request reads in c64)
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
@@ -166,12 +238,10 @@ struct Ctx {
   int64_t n_req = -1;
   DevBuf d_ia, d_ib, d_acc, d_partial, d_gidx;
   // tree buffers
-  std::vector<DevBuf> lvl_a, lvl_b, lvl_parent, lvl_digit;
-  std::vector<PinnedBuf> lvl_stage;
-  std::vector<cudaEvent_t> lvl_event;
-  DevBuf d_weights;
-  PinnedBuf weights_stage;
-  cudaEvent_t weights_event = nullptr;
+  std::vector<DevBuf> lvl_a, lvl_b;
+  Ring ring;                          // node tables + leaf weights staging
+  const double* cur_weights = nullptr;  // device leaf weights of the current leaf chunk
+  int async_run = 0;  // option: gs_run with a device output returns without a stream sync
   // run state
   gs_stats st{};
   int32_t x_p = 0;
@@ -1029,8 +1099,8 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
     j.init_zero = init_zero ? 1 : 0;
     if (pp.fused_gather) {
       j.aleaf = c.leaf_out[0].p;
-      j.ia = reinterpret_cast<const int32_t*>(c.d_ia.p);
-      j.weights = reinterpret_cast<const double*>(c.d_weights.p);
+      j.ia = reinterpret_cast<const int32_t*>(c.d_bia.p);  // A index per bucket slot
+      j.weights = c.cur_weights;
       j.bstart = reinterpret_cast<const int32_t*>(c.d_bstart.p);
       j.breq = reinterpret_cast<const int32_t*>(c.d_breq.p);
       j.btl = reinterpret_cast<const int32_t*>(c.d_btl.p);
@@ -1106,14 +1176,12 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
 // leaf multiplicities (duplicate prefixes / branch ranges collapsed into one node)
 static void upload_weights(Ctx& c, const Node* nodes, int64_t n) {
   if (c.host_only || n == 0) return;
-  c.weights_stage.ensure(n * sizeof(double));
-  cudaEventSynchronize(c.weights_event);
-  double* w = reinterpret_cast<double*>(c.weights_stage.p);
+  const size_t off = c.ring.alloc(n * sizeof(double));
+  double* w = reinterpret_cast<double*>(c.ring.h(off));
   for (int64_t j = 0; j < n; ++j) w[j] = (double)((nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0));
-  c.d_weights.ensure(std::max<size_t>(n * sizeof(double), 16));
-  CK(cudaMemcpyAsync(c.d_weights.p, w, n * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+  c.ring.commit(off, n * sizeof(double), c.stream);
+  c.cur_weights = reinterpret_cast<const double*>(c.ring.d(off));
   c.st.h2d_bytes += 8.0 * n;
-  CK(cudaEventRecord(c.weights_event, c.stream));
   if (c.fused_active) {  // partials of the fused leaf gather, one row per group of 8 leaves
     const size_t groups = (size_t)((n + 7) / 8);
     c.d_partial.ensure(std::max<size_t>(groups * (size_t)std::max<int64_t>(c.n_req, 1) * sizeof(double2), 16));
@@ -1167,7 +1235,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     auto kern = GL == 3 ? gather_grouped_kernel<R, 3> : gather_grouped_kernel<R, 2>;
     kern<<<dim3((unsigned)xblocks, (unsigned)gy), threads, 0, c.stream>>>(
         c.leaf_out[0].p, c.leaf_out[1].p, 1LL << qa, 1LL << qb, (int)n, (int)per_y,
-        reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const int32_t*>(c.d_ia.p),
+        c.cur_weights, reinterpret_cast<const int32_t*>(c.d_ia.p),
         reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
     launch_check("gather_grouped_kernel", xblocks * gy, threads, 0);
     groups = gy;
@@ -1189,7 +1257,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     }
     gather_smem_kernel<R, RPT><<<dim3((unsigned)xb, (unsigned)g), NT, 2 * pair_bytes, c.stream>>>(
         c.lvl_a[l].p, c.lvl_b[l].p, qa, qb, (int)n, (int)per2,
-        reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const uint32_t*>(c.d_packed.p),
+        c.cur_weights, reinterpret_cast<const uint32_t*>(c.d_packed.p),
         nreq, (int)req_per_cta, reinterpret_cast<double2*>(c.d_partial.p));
     launch_check("gather_smem_kernel", xb * g, NT, 2 * pair_bytes);
     groups = g;
@@ -1197,7 +1265,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   dim3 grid((unsigned)xblocks, (unsigned)groups);
   gather_kernel<R><<<grid, threads, 0, c.stream>>>(
       c.lvl_a[l].p, c.lvl_b[l].p, 1LL << qa, 1LL << qb, (int)n, (int)per,
-      reinterpret_cast<const double*>(c.d_weights.p), reinterpret_cast<const int32_t*>(c.d_ia.p),
+      c.cur_weights, reinterpret_cast<const int32_t*>(c.d_ia.p),
       reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
   launch_check("gather_kernel", xblocks * groups, threads, 0);
   }
@@ -1229,21 +1297,21 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
   for (int64_t s = 0; s < (int64_t)kids.size(); s += cap) {
     const int64_t n = std::min<int64_t>(cap, (int64_t)kids.size() - s);
     const Node* chunk = kids.data() + s;
+    const uint64_t* d_digit = nullptr;
+    const int32_t* d_parent = nullptr;
     if (!c.host_only) {
-      PinnedBuf& stg = c.lvl_stage[l + 1];
-      cudaEventSynchronize(c.lvl_event[l + 1]);
-      uint64_t* hd = reinterpret_cast<uint64_t*>(stg.p);
+      const size_t off = c.ring.alloc(n * 12);
+      uint64_t* hd = reinterpret_cast<uint64_t*>(c.ring.h(off));
       int32_t* hp = reinterpret_cast<int32_t*>(hd + n);
       for (int64_t j = 0; j < n; ++j) hd[j] = chunk[j].digit, hp[j] = chunk[j].parent;
-      CK(cudaMemcpyAsync(c.lvl_digit[l + 1].p, hd, n * 8, cudaMemcpyHostToDevice, c.stream));
-      CK(cudaMemcpyAsync(c.lvl_parent[l + 1].p, hp, n * 4, cudaMemcpyHostToDevice, c.stream));
+      c.ring.commit(off, n * 12, c.stream);
+      d_digit = reinterpret_cast<const uint64_t*>(c.ring.d(off));
+      d_parent = reinterpret_cast<const int32_t*>(d_digit + n);
       c.st.h2d_bytes += 12.0 * n;
-      CK(cudaEventRecord(c.lvl_event[l + 1], c.stream));
     }
     if (l + 1 == D) upload_weights(c, chunk, n);  // the fused leaf pass reads them
     run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
-                        at(c.lvl_b, l + 1), reinterpret_cast<const int32_t*>(at(c.lvl_parent, l + 1)),
-                        reinterpret_cast<const uint64_t*>(at(c.lvl_digit, l + 1)), false);
+                        at(c.lvl_b, l + 1), d_parent, d_digit, false);
     descend<R>(c, l + 1, chunk, n);
   }
 }
@@ -1298,14 +1366,10 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
   if (c.host_only) return;
   c.lvl_a.resize(D + 1);
   c.lvl_b.resize(D + 1);
-  c.lvl_parent.resize(D + 1);
-  c.lvl_digit.resize(D + 1);
-  c.lvl_stage.resize(D + 1);
-  while ((int)c.lvl_event.size() < D + 1) {
-    cudaEvent_t e;
-    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c.lvl_event.push_back(e);
-  }
+  int64_t max_cap = 1;
+  for (int l = 0; l <= D; ++l) max_cap = std::max(max_cap, c.cap[l]);
+  // one chunk's digits + parents + weights, several times over, at least 32 MiB
+  c.ring.reserve(std::max<size_t>((size_t)32 << 20, (size_t)max_cap * 20 * 4 + 4096), c.stream);
   // release oversized buffers first so growing one level cannot overshoot the budget
   for (int l = 0; l <= D; ++l) {
     if (c.lvl_a[l].bytes > (size_t)c.cap[l] * ((size_t)1 << p.q[0]) * c.esize()) c.lvl_a[l].release();
@@ -1314,11 +1378,7 @@ static void plan_buffers(Ctx& c, int64_t n_leaves) {
   for (int l = 0; l <= D; ++l) {
     c.lvl_a[l].ensure((size_t)c.cap[l] * ((size_t)1 << p.q[0]) * c.esize());
     c.lvl_b[l].ensure((size_t)c.cap[l] * ((size_t)1 << p.q[1]) * c.esize());
-    c.lvl_parent[l].ensure(c.cap[l] * 4 + 16);
-    c.lvl_digit[l].ensure(c.cap[l] * 8 + 16);
-    c.lvl_stage[l].ensure(c.cap[l] * 12 + 16);
   }
-  if (!c.weights_event) CK(cudaEventCreateWithFlags(&c.weights_event, cudaEventDisableTiming));
   if (c.grouped_leaf) {
     const size_t gsz = (size_t)1 << c.group_log;
     const size_t slots = (size_t)((c.cap[D] + gsz - 1) / gsz) * gsz;
@@ -1342,6 +1402,7 @@ static void build_buckets(Ctx& c) {
   c.d_bstart.ensure((size_t)(tiles + 1) * 4);
   c.d_breq.ensure(std::max<size_t>((size_t)n * 4, 16));
   c.d_btl.ensure(std::max<size_t>((size_t)n * 4, 16));
+  c.d_bia.ensure(std::max<size_t>((size_t)n * 4, 16));
   int32_t* cnt = reinterpret_cast<int32_t*>(c.d_bcount.p);
   int32_t* start = reinterpret_cast<int32_t*>(c.d_bstart.p);
   CK(cudaMemsetAsync(cnt, 0, (size_t)(tiles + 1) * 4, c.stream));
@@ -1354,9 +1415,10 @@ static void build_buckets(Ctx& c) {
   CK(cub::DeviceScan::ExclusiveSum(c.d_cubtmp.p, tmp, cnt, start, tiles + 1, c.stream));
   CK(cudaMemcpyAsync(cnt, start, (size_t)(tiles + 1) * 4, cudaMemcpyDeviceToDevice, c.stream));
   if (n > 0)
-    bucket_fill_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const int32_t*>(c.d_ib.p), n, m, cnt,
-                                                     reinterpret_cast<int32_t*>(c.d_breq.p),
-                                                     reinterpret_cast<int32_t*>(c.d_btl.p));
+    bucket_fill_kernel<<<blocks, 256, 0, c.stream>>>(
+        reinterpret_cast<const int32_t*>(c.d_ib.p), reinterpret_cast<const int32_t*>(c.d_ia.p), n, m, cnt,
+        reinterpret_cast<int32_t*>(c.d_breq.p), reinterpret_cast<int32_t*>(c.d_btl.p),
+        reinterpret_cast<int32_t*>(c.d_bia.p));
   CK(cudaGetLastError());
   c.bucket_valid = true;
 }
@@ -1461,8 +1523,6 @@ void gs_destroy(gs_ctx* ctx) {
   if (!ctx->c.host_only) {
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
-    for (auto e : ctx->c.lvl_event) cudaEventDestroy(e);
-    if (ctx->c.weights_event) cudaEventDestroy(ctx->c.weights_event);
     if (ctx->c.ev0) cudaEventDestroy(ctx->c.ev0);
     if (ctx->c.ev1) cudaEventDestroy(ctx->c.ev1);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
@@ -1475,8 +1535,13 @@ const char* gs_last_error(const gs_ctx* ctx) { return ctx ? ctx->c.err.c_str() :
 
 int gs_set_stream(gs_ctx* ctx, void* s) {
   if (!ctx) return GS_ERR_ARG;
-  ctx->c.stream = s ? reinterpret_cast<cudaStream_t>(s) : ctx->c.own_stream;
-  return GS_OK;
+  // staging regions are recycled in stream order: finish the old stream's work first
+  GS_GUARD(ctx, {
+    Ctx& c = ctx->c;
+    if (!c.host_only && c.stream) CK(cudaStreamSynchronize(c.stream));
+    c.ring.drain();
+    c.stream = s ? reinterpret_cast<cudaStream_t>(s) : c.own_stream;
+  });
 }
 
 int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
@@ -1510,6 +1575,8 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "smem_gather") {
       c.smem_gather = value ? 1 : 0;
+    } else if (k == "async_run") {
+      c.async_run = value ? 1 : 0;
     } else if (k == "jit") {
       c.use_jit = value ? 1 : 0;
       if (c.have_prog) gs::jit_program(c);
@@ -1737,10 +1804,14 @@ int gs_run(gs_ctx* ctx, int32_t x_p, int64_t n_prefix, const int64_t* prefixes, 
         CK(cudaMemcpyAsync(out_host, c.d_acc.p, c.n_req * sizeof(double2), cudaMemcpyDeviceToHost, c.stream));
         c.st.d2h_bytes += 16.0 * c.n_req;
       }
-      CK(cudaStreamSynchronize(c.stream));
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
-      c.st.ms_total = ms;
+      if (c.async_run && !out_host) {
+        c.st.ms_total = -1;  // still running: the caller orders on the stream
+      } else {
+        CK(cudaStreamSynchronize(c.stream));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+        c.st.ms_total = ms;
+      }
     } else if (out_host) {
       std::fill(out_host, out_host + 2 * std::max<int64_t>(c.n_req, 0), 0.0);
     }

@@ -416,8 +416,8 @@ static __global__ void bucket_count_kernel(const int32_t* ib, long long n, const
   atomicAdd(count + t, 1);
 }
 
-static __global__ void bucket_fill_kernel(const int32_t* ib, long long n, const BucketMap m, int32_t* cursor,
-                                          int32_t* breq, int32_t* btl) {
+static __global__ void bucket_fill_kernel(const int32_t* ib, const int32_t* ia, long long n, const BucketMap m,
+                                          int32_t* cursor, int32_t* breq, int32_t* btl, int32_t* bia) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   unsigned t, l;
@@ -425,6 +425,7 @@ static __global__ void bucket_fill_kernel(const int32_t* ib, long long n, const 
   const int pos = atomicAdd(cursor + t, 1);
   breq[pos] = (int32_t)i;
   btl[pos] = (int32_t)l;
+  bia[pos] = ia[i];
 }
 
 }  // namespace gs

@@ -164,3 +164,48 @@ def test_cfg5_reference_paths(ps, name):
     circ, plan, _, _ = configs.build(name, n_req=4)
     for pid, want in zip(g["path_ids"], g["path_amps"]):
         assert rel_l2(ps.run_path(circ, plan, int(pid), g["requests"]).amps, want) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg2h"])
+def test_fused_leaf_gather_option(ps, name):
+    """fuse_gather=1 (gather inside the last B-side leaf pass) gives the same sums."""
+    g = load_amps(name)
+    circ, plan, _, _ = configs.build(name, n_req=4)
+    eng = _engine("c64")
+    eng.set_option("fuse_gather", 1)
+    try:
+        got = ps.run_batched(circ, plan, g["requests"], prefixes=g["prefixes"]).amps
+    finally:
+        eng.set_option("fuse_gather", 0)
+    assert rel_l2(got, g["amps_c64"]) <= C64_TOL
+
+
+def test_async_run_stream_order(ps):
+    """async_run=1: back-to-back runs into a device buffer, read after one sync,
+    equal the synchronous results (staging ring reuse across queued runs)."""
+    import torch
+
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build("cfg3", n_req=64)
+    eng = _engine("c64")
+    eng.load_program(lowered(circ, plan.cut))
+    eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+    wins = [pre[i * 96:(i + 1) * 96] for i in range(6)]
+    want = [ps.run_batched(circ, plan, req, prefixes=w).amps for w in wins]
+    eng.load_program(lowered(circ, plan.cut))
+    eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+    outs = [torch.zeros(2 * req.size, dtype=torch.float64, device="cuda:0") for _ in wins]
+    stream = torch.cuda.Stream()
+    eng.set_stream(stream.cuda_stream)
+    eng.set_option("async_run", 1)
+    try:
+        for w, o in zip(wins, outs):
+            eng.run(plan.x_p, w, 0, plan.branch_space, out_device_ptr=o.data_ptr(), want_host=False)
+        stream.synchronize()
+    finally:
+        eng.set_option("async_run", 0)
+        eng.set_stream(None)
+    for o, w in zip(outs, want):
+        got = o.cpu().numpy().view(np.complex128)
+        assert rel_l2(got, w) <= 1e-12
