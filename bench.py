@@ -279,7 +279,9 @@ def main():
         dist.barrier()
     stats = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clk = ClockSampler(local).start()
+    clk = ClockSampler(local, int(os.environ.get("GS_BENCH_CLOCK_MS", "20")))
+    if os.environ.get("GS_BENCH_NO_CLOCKS") != "1":  # diagnostics only: the JSON then says "unsampled"
+        clk.start()
     torch.cuda.synchronize()
     clk.mark(True)
     e0.record(stream)

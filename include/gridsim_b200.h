@@ -81,6 +81,8 @@ typedef struct gs_stats {
   double pass_bytes_min;     /* one read+write per level per node (roofline) */
   double h2d_bytes;          /* host->device bytes copied by this gs_run     */
   double d2h_bytes;          /* device->host bytes copied by this gs_run     */
+  double host_ms_enqueue;    /* host time to plan + enqueue the whole run    */
+  double host_ms_max_gap;    /* longest host interval between two launches   */
 } gs_stats;
 
 int gs_abi_version(void);

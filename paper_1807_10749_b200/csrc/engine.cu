@@ -228,6 +228,8 @@ struct Ctx {
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
   int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
   int use_jit = 1;   // specialise passes at load time (NVRTC); interpreter otherwise
+  int vec_hbm = 1;   // option: vector (16-byte) HBM stage layouts for specialised passes
+  int jit_min_blocks = 3;  // option: __launch_bounds__ min CTAs/SM of specialised passes (0 = none)
   std::vector<JitModule*> jit_mods;   // one per compile chunk
   std::vector<std::pair<int, int>> jit_loc;  // pass jit_index -> (module, kernel)
   JitModule* jit = nullptr;           // non-null when any module is loaded
@@ -252,6 +254,17 @@ struct Ctx {
   std::vector<int> lvl_end;        // digit end e_l per level
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<std::vector<Node>> kids;  // per-level child scratch for the DFS
+  std::chrono::steady_clock::time_point last_tick;
+  uint64_t sched_serial = 0;       // bumped by every (re)schedule of the program
+  std::vector<int64_t> plan_key;   // inputs of the current buffer plan
+  // host-side pacing: longest interval between consecutive kernel launches
+  const char* gap_label = "";
+  void tick(const char* label = "launch") {
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - last_tick).count();
+    if (ms > st.host_ms_max_gap) st.host_ms_max_gap = ms, gap_label = label;
+    last_tick = now;
+  }
 
   size_t esize() const { return precision == GS_C64 ? 8 : 16; }
   int kmax() const {
@@ -597,6 +610,7 @@ static uint64_t pack_level_digits(const Program& p, int l, int64_t v);
 
 static void schedule_program(Ctx& c) {
   Program& p = c.prog;
+  ++c.sched_serial;
   c.host_devops.clear();
   // Leaf states go to the grouped path-minor layout when the gather reads them
   // from HBM (half-states too large for the shared-memory gather).
@@ -674,7 +688,9 @@ static void schedule_program(Ctx& c) {
         // tile = k state bits + slot bits batching small states, up to 2^13 (c64) /
         // 2^12 (c128) amplitudes and 256 threads
         pp.K = std::max(pp.k, std::min(c.kmax(), pp.M + 8));
-        pp.stages = schedule_stages(pp, pp.M);
+        // complex64 specialised passes use 16-byte HBM accesses (jitgen.inc)
+        const bool vec = c.precision == GS_C64 && c.use_jit && c.vec_hbm && pp.M == 5;
+        pp.stages = schedule_stages(pp, pp.M, vec, pp.grouped_store ? c.group_log : 0);
         pp.dev_stage_offset = (int64_t)c.host_pstages.size();
         pp.goff_offset = (int64_t)c.host_gofftab.size();
         for (int t = 0; t < (1 << pp.k); ++t) {
@@ -808,85 +824,120 @@ static void jit_program(Ctx& c) {
     c.jit_status = "off";
     return;
   }
-  // one kernel source per eligible pass
-  std::vector<std::string> kernels;
+  // one kernel per eligible pass
   std::vector<PassPlan*> order;
   for (Level& L : c.prog.levels)
     for (int side = 0; side < 2; ++side)
-      for (PassPlan& pp : L.passes[side]) {
-        if (pp.M != 5 || pp.stages.empty()) continue;
-        size_t smem = 0;
-        const int local = 0;  // renamed per chunk below
-        kernels.push_back(jitgen::pass_kernel(c, pp, local, smem, pp.fused_gather));
-        c.jit_smem.push_back(smem);
-        order.push_back(&pp);
-      }
-  const int n = (int)kernels.size();
+      for (PassPlan& pp : L.passes[side])
+        if (pp.M == 5 && !pp.stages.empty()) order.push_back(&pp);
+  const int n = (int)order.size();
   if (n == 0) {
     c.jit_status = "no eligible passes";
     return;
   }
-  // chunks compiled concurrently: ~source-size balanced, up to the core count
-  const int hw = std::max(1u, std::thread::hardware_concurrency());
-  const int n_chunks = std::max(1, std::min(n, std::min(hw, 32)));
-  std::vector<std::string> src(n_chunks, jitgen::prelude());
-  std::vector<std::vector<int>> members(n_chunks);
-  std::vector<size_t> load(n_chunks, 0);
-  std::vector<int> by_size(n);
-  for (int i = 0; i < n; ++i) by_size[i] = i;
-  std::sort(by_size.begin(), by_size.end(), [&](int x, int y) { return kernels[x].size() > kernels[y].size(); });
-  for (int i : by_size) {
-    const int ch = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    const int local = (int)members[ch].size();
-    // kernel text was generated as gsj_0: rename to its index inside the chunk
-    std::string k = kernels[i];
-    const size_t at = k.find("gsj_0(");
-    k.replace(at, 6, "gsj_" + std::to_string(local) + "(");
-    src[ch] += k;
-    members[ch].push_back(i);
-    load[ch] += k.size();
-  }
-  if (const char* dump = std::getenv("GS_JIT_DUMP")) {  // diagnostics: write the generated chunks
+  c.jit_smem.assign(n, 0);
+  c.jit_loc.assign(n, {0, 0});
+  // compile passes `ids` with a register bound for `min_blocks` CTAs/SM, in
+  // chunks compiled concurrently (~source-size balanced, up to the core count)
+  auto compile = [&](const std::vector<int>& ids, int min_blocks, std::string& err) -> bool {
+    std::vector<std::string> kernels(ids.size());
+    for (size_t t = 0; t < ids.size(); ++t) {
+      PassPlan& pp = *order[ids[t]];
+      size_t smem = 0;
+      kernels[t] = jitgen::pass_kernel(c, pp, 0, smem, pp.fused_gather, min_blocks);
+      c.jit_smem[ids[t]] = smem;
+    }
+    const int m = (int)ids.size();
+    const int hw = std::max(1u, std::thread::hardware_concurrency());
+    const int n_chunks = std::max(1, std::min(m, std::min(hw, 32)));
+    std::vector<std::string> src(n_chunks, jitgen::prelude());
+    std::vector<std::vector<int>> members(n_chunks);
+    std::vector<size_t> load(n_chunks, 0);
+    std::vector<int> by_size(m);
+    for (int i = 0; i < m; ++i) by_size[i] = i;
+    std::sort(by_size.begin(), by_size.end(), [&](int x, int y) { return kernels[x].size() > kernels[y].size(); });
+    for (int i : by_size) {
+      const int ch = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      const int local = (int)members[ch].size();
+      // kernel text was generated as gsj_0: rename to its index inside the chunk
+      std::string k = kernels[i];
+      const size_t at = k.find("gsj_0(");
+      k.replace(at, 6, "gsj_" + std::to_string(local) + "(");
+      src[ch] += k;
+      members[ch].push_back(i);
+      load[ch] += k.size();
+    }
+    if (const char* dump = std::getenv("GS_JIT_DUMP")) {  // diagnostics: write the generated chunks
+      for (int ch = 0; ch < n_chunks; ++ch)
+        if (FILE* f = std::fopen((std::string(dump) + "." + std::to_string(min_blocks) + "." + std::to_string(ch) +
+                                  ".cu").c_str(), "w")) {
+          std::fwrite(src[ch].data(), 1, src[ch].size(), f);
+          std::fclose(f);
+        }
+    }
+    if (c.host_only) {
+      size_t bytes = 0;
+      for (auto& t : src) bytes += t.size();
+      err = "generated " + std::to_string(m) + " kernels in " + std::to_string(n_chunks) + " modules (" +
+            std::to_string(bytes) + " bytes of source); not compiled on a host-only context";
+      return false;
+    }
+    std::vector<JitModule*> mods(n_chunks, nullptr);
+    std::vector<std::string> errs(n_chunks);
+    const int dev = c.device;
+    std::vector<std::thread> pool;
     for (int ch = 0; ch < n_chunks; ++ch)
-      if (FILE* f = std::fopen((std::string(dump) + "." + std::to_string(ch) + ".cu").c_str(), "w")) {
-        std::fwrite(src[ch].data(), 1, src[ch].size(), f);
-        std::fclose(f);
+      pool.emplace_back([&, ch] {
+        cudaSetDevice(dev);
+        mods[ch] = jit_compile(src[ch], (int)members[ch].size(), "gridsim_passes_" + std::to_string(ch), errs[ch]);
+      });
+    for (auto& t : pool) t.join();
+    for (int ch = 0; ch < n_chunks; ++ch)
+      if (!mods[ch]) {
+        for (JitModule* md : mods) jit_release(md);
+        err = "interpreter (jit failed: " + errs[ch].substr(0, 300) + ")";
+        return false;
       }
-  }
-  if (c.host_only) {
-    size_t bytes = 0;
-    for (auto& t : src) bytes += t.size();
-    c.jit_status = "generated " + std::to_string(n) + " kernels in " + std::to_string(n_chunks) + " modules (" +
-                   std::to_string(bytes) + " bytes of source); not compiled on a host-only context";
+    for (int ch = 0; ch < n_chunks; ++ch) {
+      const int mi = (int)c.jit_mods.size();
+      c.jit_mods.push_back(mods[ch]);
+      for (size_t k = 0; k < members[ch].size(); ++k) c.jit_loc[ids[members[ch][k]]] = {mi, (int)k};
+    }
+    return true;
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<int> all(n);
+  for (int i = 0; i < n; ++i) all[i] = i;
+  std::string err;
+  if (!compile(all, c.jit_min_blocks, err)) {
+    for (JitModule* md : c.jit_mods) jit_release(md);
+    c.jit_mods.clear();
+    c.jit_status = err;
     return;
   }
-  const auto t0 = std::chrono::steady_clock::now();
-  std::vector<JitModule*> mods(n_chunks, nullptr);
-  std::vector<std::string> errs(n_chunks);
-  const int dev = c.device;
-  std::vector<std::thread> pool;
-  for (int ch = 0; ch < n_chunks; ++ch)
-    pool.emplace_back([&, ch] {
-      cudaSetDevice(dev);
-      mods[ch] = jit_compile(src[ch], (int)members[ch].size(), "gridsim_passes_" + std::to_string(ch), errs[ch]);
-    });
-  for (auto& t : pool) t.join();
-  c.jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  for (int ch = 0; ch < n_chunks; ++ch)
-    if (!mods[ch]) {
-      for (JitModule* m : mods) jit_release(m);
-      c.jit_status = "interpreter (jit failed: " + errs[ch].substr(0, 300) + ")";
+  // a register bound that forces spills costs more than the occupancy it buys:
+  // recompile those passes unbounded
+  int n_spill = 0;
+  if (c.jit_min_blocks > 0) {
+    std::vector<int> spill;
+    for (int i = 0; i < n; ++i)
+      if (jit_local_bytes(c.jit_mods[c.jit_loc[i].first], c.jit_loc[i].second) > 0) spill.push_back(i);
+    n_spill = (int)spill.size();
+    if (!spill.empty() && !compile(spill, 0, err)) {
+      for (JitModule* md : c.jit_mods) jit_release(md);
+      c.jit_mods.clear();
+      c.jit_status = err;
       return;
     }
-  c.jit_mods = mods;
-  c.jit = mods[0];
-  c.jit_loc.assign(n, {0, 0});
-  for (int ch = 0; ch < n_chunks; ++ch)
-    for (size_t k = 0; k < members[ch].size(); ++k) c.jit_loc[members[ch][k]] = {ch, (int)k};
+  }
+  c.jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  c.jit = c.jit_mods[0];
+  const int n_chunks = (int)c.jit_mods.size();
   for (int i = 0; i < n; ++i) order[i]->jit_index = i;
   for (PassPlan* pp : order) c.fused_active |= pp->fused_gather;
-  c.jit_status = "jit: " + std::to_string(n) + " pass kernels, " + std::to_string(n_chunks) +
-                 " modules compiled in " + std::to_string(c.jit_seconds) + " s";
+  c.jit_status = "jit: " + std::to_string(n) + " pass kernels (" + std::to_string(n_spill) +
+                 " recompiled without the register bound), " + std::to_string(n_chunks) + " modules compiled in " +
+                 std::to_string(c.jit_seconds) + " s";
 }
 
 static void upload_program(Ctx& c) {
@@ -1158,6 +1209,7 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
   for (int side = 0; side < 2; ++side) {
     bool first = true;
     for (const PassPlan& pp : L.passes[side]) {
+      c.tick("pass launch");
       void* out = pp.grouped_store ? c.leaf_out[side].p : dsts[side];
       if (c.kernel_version == 2 && pp.M > 0)
         launch_pass2<R>(c, side, pp, first ? srcs[side] : dsts[side], out,
@@ -1193,6 +1245,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   for (int64_t j = 0; j < n; ++j) w_total += (nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0);
   c.st.n_paths += w_total;
   if (c.host_only || c.n_req == 0) return;
+  c.tick("gather");
   Timer t(c, &c.st.ms_gather);
   const int64_t nreq = c.n_req;
   if (c.fused_active) {  // partials were written by the fused leaf pass
@@ -1291,7 +1344,9 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
   }
   std::vector<Node>& kids = c.kids[l + 1];  // per-level scratch, reused across chunks
   kids.clear();
+  c.tick("before enumerate");
   enumerate_children(c, l, nodes, n_nodes, kids);
+  c.tick("enumerate_children");
   const int64_t cap = c.cap[l + 1];
   auto at = [](std::vector<DevBuf>& v, int i) -> void* { return i < (int)v.size() ? v[i].p : nullptr; };
   for (int64_t s = 0; s < (int64_t)kids.size(); s += cap) {
@@ -1300,11 +1355,14 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
     const uint64_t* d_digit = nullptr;
     const int32_t* d_parent = nullptr;
     if (!c.host_only) {
+      c.tick("before ring");
       const size_t off = c.ring.alloc(n * 12);
+      c.tick("ring.alloc");
       uint64_t* hd = reinterpret_cast<uint64_t*>(c.ring.h(off));
       int32_t* hp = reinterpret_cast<int32_t*>(hd + n);
       for (int64_t j = 0; j < n; ++j) hd[j] = chunk[j].digit, hp[j] = chunk[j].parent;
       c.ring.commit(off, n * 12, c.stream);
+      c.tick("ring.commit");
       d_digit = reinterpret_cast<const uint64_t*>(c.ring.d(off));
       d_parent = reinterpret_cast<const int32_t*>(d_digit + n);
       c.st.h2d_bytes += 12.0 * n;
@@ -1316,7 +1374,19 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
   }
 }
 
+static void plan_buffers_impl(Ctx& c, int64_t n_leaves);
+// The buffer plan depends only on the schedule, the leaf bound, the request
+// count and the options below; re-planning queries free device memory, which
+// can stall the host for milliseconds, so steady-state runs reuse the plan.
 static void plan_buffers(Ctx& c, int64_t n_leaves) {
+  const std::vector<int64_t> key = {n_leaves, c.n_req, c.mem_budget_mb, (int64_t)c.sched_serial,
+                                    c.fused_active ? 1 : 0, c.group_log, c.grouped_leaf ? 1 : 0, c.max_chunk,
+                                    c.host_only ? 1 : 0};
+  if (key == c.plan_key) return;
+  plan_buffers_impl(c, n_leaves);
+  c.plan_key = key;
+}
+static void plan_buffers_impl(Ctx& c, int64_t n_leaves) {
   const Program& p = c.prog;
   const int D = (int)p.levels.size() - 1;
   const double pair = (double)((1LL << p.q[0]) + (1LL << p.q[1])) * (double)c.esize();
@@ -1575,11 +1645,18 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "smem_gather") {
       c.smem_gather = value ? 1 : 0;
+    } else if (k == "vec_hbm") {
+      c.vec_hbm = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "jit_min_blocks") {
+      if (value < 0 || value > 8) throw GsError(GS_ERR_ARG, "jit_min_blocks must be 0..8");
+      c.jit_min_blocks = (int)value;
+      if (c.have_prog) gs::jit_program(c);
     } else if (k == "async_run") {
       c.async_run = value ? 1 : 0;
     } else if (k == "jit") {
-      c.use_jit = value ? 1 : 0;
-      if (c.have_prog) gs::jit_program(c);
+      c.use_jit = value ? 1 : 0;  // the HBM stage layout depends on it: reschedule
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "reg_bits") {
       if (value != 4 && value != 5) throw GsError(GS_ERR_ARG, "reg_bits must be 4 or 5");
       c.reg_bits = (int)value;
@@ -1645,7 +1722,16 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
             const gs::PStage& ps = c.host_pstages[pp.dev_stage_offset + si];
             js += (si ? ", " : "") + std::to_string(ps.op_end - ps.op_begin);
           }
-          js += "], \"store_scale\": " + std::to_string(pp.store_scale) + "}";
+          js += "], \"rb\": [";
+          for (size_t si = 0; si < pp.stages.size(); ++si) {
+            js += si ? ", [" : "[";
+            for (size_t i = 0; i < pp.stages[si].rb.size(); ++i)
+              js += (i ? ", " : "") + std::to_string(pp.stages[si].rb[i]);
+            js += "]";
+          }
+          js += "], \"lbits\": [";
+          for (size_t i = 0; i < pp.lbits.size(); ++i) js += (i ? ", " : "") + std::to_string(pp.lbits[i]);
+          js += "], \"grouped\": " + std::to_string(pp.grouped_store ? 1 : 0) + ", \"store_scale\": " + std::to_string(pp.store_scale) + "}";
         }
         js += "]}";
       }
@@ -1785,6 +1871,8 @@ int gs_run(gs_ctx* ctx, int32_t x_p, int64_t n_prefix, const int64_t* prefixes, 
     c.lvl_end.assign(p.levels.size(), 0);
     for (size_t l = 1; l < p.levels.size(); ++l) c.lvl_end[l] = p.levels[l].k_hi;
     c.st = gs_stats{};
+    const auto t_call = std::chrono::steady_clock::now();
+    c.last_tick = t_call;
     if (!c.host_only) {
       CK(cudaSetDevice(c.device));
       if (!accumulate || !out_device) {
@@ -1796,6 +1884,12 @@ int gs_run(gs_ctx* ctx, int32_t x_p, int64_t n_prefix, const int64_t* prefixes, 
     }
     if (c.precision == GS_C64) gs::run_tree<float>(c);
     else gs::run_tree<double>(c);
+    c.st.host_ms_enqueue =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
+    static const bool prof = std::getenv("GS_HOST_PROF") != nullptr;
+    if (prof && c.st.host_ms_max_gap > 1.0)
+      std::fprintf(stderr, "gs_run host gap %.3f ms ending at '%s' (enqueue %.3f ms)\n", c.st.host_ms_max_gap,
+                   c.gap_label, c.st.host_ms_enqueue);
     if (!c.host_only) {
       CK(cudaEventRecord(c.ev1, c.stream));
       if (out_device && c.n_req > 0)

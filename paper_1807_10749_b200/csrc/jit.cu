@@ -41,6 +41,7 @@ struct DriverApi {
   CUresult (*unload)(CUmodule) = nullptr;
   CUresult (*getfn)(CUfunction*, CUmodule, const char*) = nullptr;
   CUresult (*setattr)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*getattr)(int*, CUfunction_attribute, CUfunction) = nullptr;
   CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                      CUstream, void**, void**) = nullptr;
   bool ok = false;
@@ -88,6 +89,7 @@ DriverApi& driver() {
              get("cuModuleUnload", reinterpret_cast<void**>(&api.unload)) &&
              get("cuModuleGetFunction", reinterpret_cast<void**>(&api.getfn)) &&
              get("cuFuncSetAttribute", reinterpret_cast<void**>(&api.setattr)) &&
+             get("cuFuncGetAttribute", reinterpret_cast<void**>(&api.getattr)) &&
              get("cuLaunchKernel", reinterpret_cast<void**>(&api.launch));
     if (!api.ok) {
       cudaGetLastError();
@@ -202,6 +204,12 @@ static JitModule* load_cubin(const std::vector<char>& cubin, int n_kernels, std:
     }
   }
   return m.release();
+}
+
+int jit_local_bytes(JitModule* m, int idx) {
+  int v = 0;
+  if (driver().getattr(&v, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, m->fns[idx]) != CUDA_SUCCESS) return -1;
+  return v;
 }
 
 void jit_release(JitModule* m) {

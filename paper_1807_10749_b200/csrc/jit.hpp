@@ -48,6 +48,8 @@ struct JitModule;
 // compile `source` (kernels gsj_0 .. gsj_{n-1}); returns nullptr with `err` set on failure
 JitModule* jit_compile(const std::string& source, int n_kernels, const std::string& tag, std::string& err);
 void jit_release(JitModule* m);
+// thread-local memory (register spills) of kernel `idx`, bytes; -1 if unknown
+int jit_local_bytes(JitModule* m, int idx);
 // launch kernel `idx` of the module
 cudaError_t jit_launch(JitModule* m, int idx, unsigned grid, unsigned block, size_t smem, cudaStream_t s,
                        const JArgs& args, std::string& err);

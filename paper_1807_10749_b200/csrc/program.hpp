@@ -162,20 +162,33 @@ inline std::vector<PassPlan> schedule_passes(const std::vector<HostOp>& ops, int
 // run in any stage (its other bits are thread- or tile-uniform).  Stage 0
 // and the last stage keep tile bits 0..4 on the lanes (when the tile has room)
 // so the HBM load and store are warp-contiguous.
-inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M) {
+// HBM-facing stages (the first loads, the last stores) keep low tile bits on
+// the lanes so every warp access is made of contiguous runs.  Classic layout
+// (vec = false): tile bits 0..4 are lanes (>= 256-byte runs at 8 bytes per
+// amplitude).  Vector layout (vec = true, complex64 specialised kernels): tile
+// bits 1 and 2 must be lanes (>= 64-byte runs: one HBM burst), tile bit 0 is
+// preferably a register bit so adjacent amplitudes move as one 16-byte access,
+// and tile bits 3 and 4 may be register bits.  A grouped store (2^G leaves
+// interleaved per amplitude, G >= 3) puts the slot bits on the lowest lanes,
+// so any last stage already writes >= 64-byte runs.
+inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M, bool vec = false, int group_log = 0) {
   const int k = pp.k;
   std::vector<int> tile_of(64, -1);
   for (int j = 0; j < k; ++j) tile_of[pp.lbits[j]] = j;
   const int lane_low = (k - 5 >= M) ? 5 : 0;
+  vec = vec && lane_low == 5;
+  // may tile bit j be a register bit of an HBM-facing stage?
+  auto hbm_ok = [&](int j) { return vec ? (j == 0 || j >= 3) : j >= lane_low; };
   std::vector<StagePlan> out;
   std::vector<HostOp> remaining = pp.ops;
+  std::vector<int> last_fill;  // register bits of the latest stage no op needs
   bool first = true;
   while (!remaining.empty() || first) {
     std::vector<char> in_r(k, 0);
     int n_r = 0;
     std::vector<char> blk_nd(k, 0), blk_d(k, 0);
     std::vector<HostOp> taken, deferred;
-    auto allowed = [&](int j) { return j >= (first ? lane_low : 0); };
+    auto allowed = [&](int j) { return !first || hbm_ok(j); };
     for (const HostOp& op : remaining) {
       const int sb[2] = {op.s0, op.s1};
       int tb[2] = {-1, -1};
@@ -216,10 +229,13 @@ inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M) {
       }
     }
     if (taken.empty() && !first) throw GsError(-1, "stage scheduler made no progress");
+    if (vec && first && n_r < M && !in_r[0]) in_r[0] = 1, ++n_r;  // 16-byte loads
+    std::vector<int> fill;
     for (int j = k - 1; j >= 0 && n_r < M; --j)
-      if (!in_r[j] && allowed(j)) in_r[j] = 1, ++n_r;
+      if (!in_r[j] && allowed(j)) in_r[j] = 1, ++n_r, fill.push_back(j);
     for (int j = k - 1; j >= 0 && n_r < M; --j)
-      if (!in_r[j]) in_r[j] = 1, ++n_r;
+      if (!in_r[j]) in_r[j] = 1, ++n_r, fill.push_back(j);
+    last_fill = fill;
     StagePlan sp;
     for (int j = 0; j < k; ++j)
       if (in_r[j]) sp.rb.push_back(j);
@@ -228,12 +244,22 @@ inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M) {
     remaining = std::move(deferred);
     first = false;
   }
-  // the store stage must leave tile bits 0..4 on the lanes
-  bool low_in_r = false;
-  for (int j : out.back().rb) low_in_r |= (j < lane_low);
-  if (low_in_r) {
+  // 16-byte stores: trade a filler register bit of the last stage for tile bit 0
+  if (vec && group_log < 3 && !last_fill.empty()) {
+    std::vector<int>& rb = out.back().rb;
+    if (std::find(rb.begin(), rb.end(), 0) == rb.end()) {
+      *std::find(rb.begin(), rb.end(), last_fill.back()) = 0;
+      std::sort(rb.begin(), rb.end());
+    }
+  }
+  // the store stage must leave the run-forming tile bits on the lanes
+  bool bad = false;
+  if (group_log < 3)
+    for (int j : out.back().rb) bad |= !hbm_ok(j);
+  if (bad) {
     StagePlan sp;
-    for (int j = k - M; j < k; ++j) sp.rb.push_back(j);
+    if (vec) sp.rb.push_back(0);
+    for (int j = k - M + (vec ? 1 : 0); j < k; ++j) sp.rb.push_back(j);
     out.push_back(std::move(sp));
   }
   return out;

@@ -58,6 +58,8 @@ class GsStats(ctypes.Structure):
         ("pass_bytes_min", ctypes.c_double),
         ("h2d_bytes", ctypes.c_double),
         ("d2h_bytes", ctypes.c_double),
+        ("host_ms_enqueue", ctypes.c_double),
+        ("host_ms_max_gap", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:
