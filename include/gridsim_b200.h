@@ -157,6 +157,18 @@ int gs_run(gs_ctx* ctx, int32_t x_p, int64_t n_prefix, const int64_t* prefixes,
            int64_t branch_lo, int64_t branch_hi, double* out_host, void* out_device,
            int32_t accumulate, gs_stats* stats);
 
+/* One call = gs_set_requests_global + gs_run: the reference's
+ * run_batched(circuit, plan, requests, prefixes) (pathsum.py:574-640) with the
+ * program already loaded.  The requests are validated and staged on host
+ * worker threads and uploaded + split on a side stream while the path tree is
+ * enqueued, so their transfer overlaps the first gate passes.  Errors as for
+ * the two calls (GS_ERR_INDEX for an index outside [0, 2^n_qubits), reported
+ * before any output is written); afterwards the requests stay loaded. */
+int gs_run_batched(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32_t n_qubits,
+                   const int32_t* block_a, const int32_t* block_b, int32_t x_p, int64_t n_prefix,
+                   const int64_t* prefixes, int64_t branch_lo, int64_t branch_hi, double* out_host,
+                   void* out_device, int32_t accumulate, gs_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -255,6 +255,29 @@ struct Ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<std::vector<Node>> kids;  // per-level child scratch for the DFS
   std::chrono::steady_clock::time_point last_tick;
+  // requests staged by gs_run_batched: host copy on worker threads while the
+  // tree is enqueued; the split runs on a side stream the first gather waits for
+  struct PendingRequests {
+    bool active = false;
+    std::vector<std::thread> workers;
+    std::vector<char> bad;  // per worker: an index outside the state space
+    int64_t n = 0;
+    SplitRuns runs{};
+    bool packed = false;
+    ~PendingRequests() { join(); }
+    void join() {
+      for (auto& t : workers)
+        if (t.joinable()) t.join();
+      workers.clear();
+    }
+  } pend;
+  PinnedBuf req_stage;
+  PinnedBuf out_stage;                 // pinned bounce buffer of the host result
+  int64_t d2h_chunk_mb = 0;            // option: pipelined result download chunk (0 = one direct copy;
+                                       // measured no faster than the driver's own staging for 16 MB)
+  std::vector<cudaEvent_t> out_events;  // one per result chunk
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t req_done = nullptr;
   uint64_t sched_serial = 0;       // bumped by every (re)schedule of the program
   std::vector<int64_t> plan_key;   // inputs of the current buffer plan
   // host-side pacing: longest interval between consecutive kernel launches
@@ -1240,10 +1263,38 @@ static void upload_weights(Ctx& c, const Node* nodes, int64_t n) {
   }
 }
 
+// Complete the requests staged by gs_run_batched: join the host copies, then
+// upload + split on the side stream -- ordered after this run's start, so an
+// earlier queued run is done with the request buffers -- and make the run's
+// stream wait for the split before its first gather.
+static void finish_requests(Ctx& c) {
+  if (!c.pend.active) return;
+  c.pend.active = false;
+  c.pend.join();
+  for (char b : c.pend.bad)
+    if (b) {
+      c.n_req = -1;
+      throw GsError(GS_ERR_INDEX, "request index outside the state space");
+    }
+  const int64_t n = c.pend.n;
+  if (c.host_only || n == 0) return;
+  CK(cudaStreamWaitEvent(c.side_stream, c.ev0, 0));
+  CK(cudaMemcpyAsync(c.d_gidx.p, c.req_stage.p, n * 8, cudaMemcpyHostToDevice, c.side_stream));
+  split_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.side_stream>>>(
+      reinterpret_cast<const long long*>(c.d_gidx.p), n, c.pend.runs, reinterpret_cast<int32_t*>(c.d_ia.p),
+      reinterpret_cast<int32_t*>(c.d_ib.p), c.pend.packed ? reinterpret_cast<uint32_t*>(c.d_packed.p) : nullptr);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c.req_done, c.side_stream));
+  CK(cudaStreamWaitEvent(c.stream, c.req_done, 0));
+  c.st.h2d_bytes += 8.0 * n;
+  c.st.n_launches += 1;
+}
+
 template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64_t n) {
   int64_t w_total = 0;
   for (int64_t j = 0; j < n; ++j) w_total += (nodes[j].i1 - nodes[j].i0) * (nodes[j].b1 - nodes[j].b0);
   c.st.n_paths += w_total;
+  finish_requests(c);
   if (c.host_only || c.n_req == 0) return;
   c.tick("gather");
   Timer t(c, &c.st.ms_gather);
@@ -1500,7 +1551,10 @@ static void run_tree(Ctx& c) {
   int64_t n_leaves_bound = (int64_t)c.prefixes.size() * (c.branch_hi - c.branch_lo);
   plan_buffers(c, std::max<int64_t>(1, n_leaves_bound));
   c.st.n_levels = D + 1;
-  if (c.fused_active && !c.host_only && !c.bucket_valid && c.n_req > 0) build_buckets(c);
+  if (c.fused_active && !c.host_only && !c.bucket_valid && c.n_req > 0) {
+    finish_requests(c);
+    build_buckets(c);
+  }
   const Node root0{0, (int64_t)c.prefixes.size(), 0, 0, c.branch_lo, c.branch_hi, 0, 0};
   if (D == 0) upload_weights(c, &root0, 1);  // the root is the leaf
   // root: |0...0> through the root segment
@@ -1596,6 +1650,12 @@ void gs_destroy(gs_ctx* ctx) {
     if (ctx->c.ev0) cudaEventDestroy(ctx->c.ev0);
     if (ctx->c.ev1) cudaEventDestroy(ctx->c.ev1);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
+    if (ctx->c.side_stream) {
+      cudaStreamSynchronize(ctx->c.side_stream);
+      cudaStreamDestroy(ctx->c.side_stream);
+    }
+    if (ctx->c.req_done) cudaEventDestroy(ctx->c.req_done);
+    for (cudaEvent_t e : ctx->c.out_events) cudaEventDestroy(e);
     for (gs::JitModule* m : ctx->c.jit_mods) gs::jit_release(m);
   }
   delete ctx;
@@ -1652,6 +1712,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (value < 0 || value > 8) throw GsError(GS_ERR_ARG, "jit_min_blocks must be 0..8");
       c.jit_min_blocks = (int)value;
       if (c.have_prog) gs::jit_program(c);
+    } else if (k == "d2h_chunk_mb") {
+      if (value < 0 || value > 1024) throw GsError(GS_ERR_ARG, "d2h_chunk_mb must be 0..1024");
+      c.d2h_chunk_mb = value;
     } else if (k == "async_run") {
       c.async_run = value ? 1 : 0;
     } else if (k == "jit") {
@@ -1749,6 +1812,58 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
   });
 }
 
+}  // extern "C"
+
+namespace gs {
+
+// bit runs of the cut: qubit q owns global bit n-1-q, local j owns bit q_blk-1-j
+static SplitRuns split_runs(const Ctx& c, int32_t n_qubits, const int32_t* block_a, const int32_t* block_b) {
+  const int qs[2] = {c.prog.q[0], c.prog.q[1]};
+  if (qs[0] + qs[1] != n_qubits || n_qubits > 62) throw GsError(GS_ERR_ARG, "cut does not match the program");
+  SplitRuns runs{};
+  runs.qa = qs[0];
+  std::vector<char> seen(n_qubits, 0);
+  for (int b = 0; b < 2; ++b) {
+    const int32_t* blk = b ? block_b : block_a;
+    int j = 0;
+    while (j < qs[b]) {
+      int k = j;
+      while (k + 1 < qs[b] && blk[k + 1] == blk[k] + 1) ++k;
+      for (int t = j; t <= k; ++t) {
+        if (blk[t] < 0 || blk[t] >= n_qubits || seen[blk[t]]) throw GsError(GS_ERR_ARG, "bad cut blocks");
+        seen[blk[t]] = 1;
+      }
+      if (runs.n[b] >= 32) throw GsError(GS_ERR_ARG, "cut has too many bit runs");
+      runs.src[b][runs.n[b]] = n_qubits - 1 - blk[k];
+      runs.width[b][runs.n[b]] = k - j + 1;
+      runs.dst[b][runs.n[b]] = qs[b] - 1 - k;
+      ++runs.n[b];
+      j = k + 1;
+    }
+  }
+  return runs;
+}
+
+static bool packed_requests(const Ctx& c) { return c.prog.q[0] + c.prog.q[1] <= 31; }
+
+static void ensure_request_buffers(Ctx& c, int64_t n_req) {
+  c.d_gidx.ensure(std::max<size_t>(n_req * 8, 16));
+  c.d_ia.ensure(std::max<size_t>(n_req * 4, 16));
+  c.d_ib.ensure(std::max<size_t>(n_req * 4, 16));
+  if (packed_requests(c)) c.d_packed.ensure(std::max<size_t>(n_req * 4, 16));
+  c.d_acc.ensure(std::max<size_t>(n_req * sizeof(double2), 16));
+}
+
+template <typename R> static void run_tree(Ctx& c);
+
+// body of gs_run / gs_run_batched (requests already loaded or staged)
+static void run_body(Ctx& c, int32_t x_p, int64_t n_prefix, const int64_t* prefixes, int64_t branch_lo,
+                     int64_t branch_hi, double* out_host, void* out_device, int32_t accumulate, gs_stats* stats);
+
+}  // namespace gs
+
+extern "C" {
+
 int gs_set_requests_global(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32_t n_qubits,
                            const int32_t* block_a, const int32_t* block_b) {
   if (!ctx) return GS_ERR_ARG;
@@ -1756,42 +1871,15 @@ int gs_set_requests_global(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32
     Ctx& c = ctx->c;
     if (!c.have_prog) throw GsError(GS_ERR_STATE, "no program loaded");
     if (n_req < 0 || (n_req > 0 && !idx) || !block_a || !block_b) throw GsError(GS_ERR_ARG, "bad request arrays");
-    const int qs[2] = {c.prog.q[0], c.prog.q[1]};
-    if (qs[0] + qs[1] != n_qubits || n_qubits > 62) throw GsError(GS_ERR_ARG, "cut does not match the program");
-    // runs of consecutive qubits; qubit q owns global bit n-1-q, local j owns bit q_blk-1-j
-    gs::SplitRuns runs{};
-    runs.qa = qs[0];
-    std::vector<char> seen(n_qubits, 0);
-    for (int b = 0; b < 2; ++b) {
-      const int32_t* blk = b ? block_b : block_a;
-      int j = 0;
-      while (j < qs[b]) {
-        int k = j;
-        while (k + 1 < qs[b] && blk[k + 1] == blk[k] + 1) ++k;
-        for (int t = j; t <= k; ++t) {
-          if (blk[t] < 0 || blk[t] >= n_qubits || seen[blk[t]]) throw GsError(GS_ERR_ARG, "bad cut blocks");
-          seen[blk[t]] = 1;
-        }
-        if (runs.n[b] >= 32) throw GsError(GS_ERR_ARG, "cut has too many bit runs");
-        runs.src[b][runs.n[b]] = n_qubits - 1 - blk[k];
-        runs.width[b][runs.n[b]] = k - j + 1;
-        runs.dst[b][runs.n[b]] = qs[b] - 1 - k;
-        ++runs.n[b];
-        j = k + 1;
-      }
-    }
+    const gs::SplitRuns runs = gs::split_runs(c, n_qubits, block_a, block_b);
     const int64_t lim = 1LL << n_qubits;
     for (int64_t i = 0; i < n_req; ++i)
       if (idx[i] < 0 || idx[i] >= lim) throw GsError(GS_ERR_INDEX, "request index outside the state space");
     c.n_req = -1;
     if (!c.host_only) {
       CK(cudaSetDevice(c.device));
-      c.d_gidx.ensure(std::max<size_t>(n_req * 8, 16));
-      c.d_ia.ensure(std::max<size_t>(n_req * 4, 16));
-      c.d_ib.ensure(std::max<size_t>(n_req * 4, 16));
-      const bool pk = qs[0] + qs[1] <= 31;
-      if (pk) c.d_packed.ensure(std::max<size_t>(n_req * 4, 16));
-      c.d_acc.ensure(std::max<size_t>(n_req * sizeof(double2), 16));
+      gs::ensure_request_buffers(c, n_req);
+      const bool pk = gs::packed_requests(c);
       if (n_req > 0) {
         CK(cudaMemcpyAsync(c.d_gidx.p, idx, n_req * 8, cudaMemcpyHostToDevice, c.stream));
         gs::split_kernel<<<(unsigned)((n_req + 255) / 256), 256, 0, c.stream>>>(
@@ -1802,6 +1890,62 @@ int gs_set_requests_global(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32
     }
     c.n_req = n_req;
     c.bucket_valid = false;
+  });
+}
+
+int gs_run_batched(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32_t n_qubits, const int32_t* block_a,
+                   const int32_t* block_b, int32_t x_p, int64_t n_prefix, const int64_t* prefixes,
+                   int64_t branch_lo, int64_t branch_hi, double* out_host, void* out_device, int32_t accumulate,
+                   gs_stats* stats) {
+  if (!ctx) return GS_ERR_ARG;
+  GS_GUARD(ctx, {
+    Ctx& c = ctx->c;
+    // worker threads never outlive the call; an unfinished staging leaves no requests loaded
+    struct Guard {
+      Ctx& c;
+      ~Guard() {
+        c.pend.join();
+        if (c.pend.active) c.pend.active = false, c.n_req = -1;
+      }
+    } guard{c};
+    if (!c.have_prog) throw GsError(GS_ERR_STATE, "no program loaded");
+    if (n_req < 0 || (n_req > 0 && !idx) || !block_a || !block_b) throw GsError(GS_ERR_ARG, "bad request arrays");
+    const gs::SplitRuns runs = gs::split_runs(c, n_qubits, block_a, block_b);
+    c.n_req = -1;
+    int64_t* stage = nullptr;
+    if (!c.host_only) {
+      CK(cudaSetDevice(c.device));
+      gs::ensure_request_buffers(c, n_req);
+      if (!c.side_stream) CK(cudaStreamCreateWithFlags(&c.side_stream, cudaStreamNonBlocking));
+      if (!c.req_done) CK(cudaEventCreateWithFlags(&c.req_done, cudaEventDisableTiming));
+      CK(cudaEventSynchronize(c.req_done));  // the previous upload has left the staging buffer
+      c.req_stage.ensure(std::max<size_t>(n_req * 8, 16));
+      stage = reinterpret_cast<int64_t*>(c.req_stage.p);
+    }
+    // validate + stage the requests on worker threads while the tree is enqueued
+    const int64_t lim = 1LL << n_qubits;
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int T = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(8, hw), (n_req + (1 << 18) - 1) >> 18));
+    c.pend.n = n_req;
+    c.pend.runs = runs;
+    c.pend.packed = gs::packed_requests(c);
+    c.pend.bad.assign(T, 0);
+    char* bad = c.pend.bad.data();
+    for (int t = 0; t < T && n_req > 0; ++t)
+      c.pend.workers.emplace_back([=] {
+        const int64_t lo = n_req * t / T, hi = n_req * (t + 1) / T;
+        bool b = false;
+        for (int64_t i = lo; i < hi; ++i) {
+          const int64_t v = idx[i];
+          b |= (v < 0) | (v >= lim);
+          if (stage) stage[i] = v;
+        }
+        bad[t] = b;
+      });
+    c.pend.active = true;
+    c.n_req = n_req;
+    c.bucket_valid = false;
+    gs::run_body(c, x_p, n_prefix, prefixes, branch_lo, branch_hi, out_host, out_device, accumulate, stats);
   });
 }
 
@@ -1843,74 +1987,128 @@ int gs_run(gs_ctx* ctx, int32_t x_p, int64_t n_prefix, const int64_t* prefixes, 
     Ctx& c = ctx->c;
     if (!c.have_prog) throw GsError(GS_ERR_STATE, "no program loaded");
     if (c.n_req < 0) throw GsError(GS_ERR_STATE, "no requests loaded");
-    const gs::Program& p = c.prog;
-    const int x = p.n_cross;
-    if (x_p < 0 || x_p > x) throw GsError(GS_ERR_PLAN, "x_p outside [0, x]");
-    if (n_prefix < 0 || (n_prefix > 0 && !prefixes)) throw GsError(GS_ERR_ARG, "bad prefix array");
-    // digit suffix products; spaces must fit int64
-    c.x_p = x_p;
-    c.S_p.assign(x_p + 1, 1);
-    for (int k = x_p - 1; k >= 0; --k) {
-      if (c.S_p[k + 1] > (1LL << 62) / p.radix[k]) throw GsError(GS_ERR_ARG, "prefix space exceeds 2^62");
-      c.S_p[k] = c.S_p[k + 1] * p.radix[k];
-    }
-    c.S_b.assign(x + 1, 1);
-    for (int k = x - 1; k >= x_p; --k) {
-      if (c.S_b[k + 1] > (1LL << 62) / p.radix[k]) throw GsError(GS_ERR_ARG, "branch space exceeds 2^62");
-      c.S_b[k] = c.S_b[k + 1] * p.radix[k];
-    }
-    const int64_t prefix_space = c.S_p[0], branch_space = c.S_b[x_p];
-    if (branch_lo < 0 || branch_hi > branch_space || branch_lo > branch_hi)
-      throw GsError(GS_ERR_ARG, "branch range outside the branch space");
-    c.prefixes.assign(prefixes, prefixes + n_prefix);
-    for (int64_t v : c.prefixes)
-      if (v < 0 || v >= prefix_space) throw GsError(GS_ERR_ARG, "prefix id outside the prefix space");
-    std::sort(c.prefixes.begin(), c.prefixes.end());
-    c.branch_lo = branch_lo;
-    c.branch_hi = branch_hi;
-    c.lvl_end.assign(p.levels.size(), 0);
-    for (size_t l = 1; l < p.levels.size(); ++l) c.lvl_end[l] = p.levels[l].k_hi;
-    c.st = gs_stats{};
-    const auto t_call = std::chrono::steady_clock::now();
-    c.last_tick = t_call;
-    if (!c.host_only) {
-      CK(cudaSetDevice(c.device));
-      if (!accumulate || !out_device) {
-        CK(cudaMemsetAsync(c.d_acc.p, 0, std::max<size_t>(c.n_req * sizeof(double2), 16), c.stream));
-      } else {
-        CK(cudaMemcpyAsync(c.d_acc.p, out_device, c.n_req * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream));
-      }
-      CK(cudaEventRecord(c.ev0, c.stream));
-    }
-    if (c.precision == GS_C64) gs::run_tree<float>(c);
-    else gs::run_tree<double>(c);
-    c.st.host_ms_enqueue =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
-    static const bool prof = std::getenv("GS_HOST_PROF") != nullptr;
-    if (prof && c.st.host_ms_max_gap > 1.0)
-      std::fprintf(stderr, "gs_run host gap %.3f ms ending at '%s' (enqueue %.3f ms)\n", c.st.host_ms_max_gap,
-                   c.gap_label, c.st.host_ms_enqueue);
-    if (!c.host_only) {
-      CK(cudaEventRecord(c.ev1, c.stream));
-      if (out_device && c.n_req > 0)
-        CK(cudaMemcpyAsync(out_device, c.d_acc.p, c.n_req * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream));
-      if (out_host && c.n_req > 0) {
-        CK(cudaMemcpyAsync(out_host, c.d_acc.p, c.n_req * sizeof(double2), cudaMemcpyDeviceToHost, c.stream));
-        c.st.d2h_bytes += 16.0 * c.n_req;
-      }
-      if (c.async_run && !out_host) {
-        c.st.ms_total = -1;  // still running: the caller orders on the stream
-      } else {
-        CK(cudaStreamSynchronize(c.stream));
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
-        c.st.ms_total = ms;
-      }
-    } else if (out_host) {
-      std::fill(out_host, out_host + 2 * std::max<int64_t>(c.n_req, 0), 0.0);
-    }
-    if (stats) *stats = c.st;
+    gs::run_body(c, x_p, n_prefix, prefixes, branch_lo, branch_hi, out_host, out_device, accumulate, stats);
   });
 }
 
 }  // extern "C"
+
+namespace gs {
+
+// Device result -> caller's (pageable) host array: chunked copies into a
+// pinned bounce buffer, each chunk moved on by a host thread as soon as its
+// copy lands, so the PCIe transfer and the host copies overlap.
+static void download_result(Ctx& c, double* out_host) {
+  const size_t bytes = (size_t)c.n_req * sizeof(double2);
+  const size_t chunk = (size_t)c.d2h_chunk_mb << 20;
+  if (chunk == 0 || bytes <= chunk) {
+    CK(cudaMemcpyAsync(out_host, c.d_acc.p, bytes, cudaMemcpyDeviceToHost, c.stream));
+    return;
+  }
+  c.out_stage.ensure(bytes);
+  const int n_chunks = (int)((bytes + chunk - 1) / chunk);
+  while ((int)c.out_events.size() < n_chunks) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.out_events.push_back(e);
+  }
+  char* stage = static_cast<char*>(c.out_stage.p);
+  const char* dev = static_cast<const char*>(c.d_acc.p);
+  for (int k = 0; k < n_chunks; ++k) {
+    const size_t off = (size_t)k * chunk, len = std::min(chunk, bytes - off);
+    CK(cudaMemcpyAsync(stage + off, dev + off, len, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaEventRecord(c.out_events[k], c.stream));
+  }
+  const int T = std::min(n_chunks, 4);
+  std::vector<std::thread> pool;
+  std::vector<char> fail(T, 0);
+  char* dst = reinterpret_cast<char*>(out_host);
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      for (int k = t; k < n_chunks; k += T) {
+        if (cudaEventSynchronize(c.out_events[k]) != cudaSuccess) {
+          fail[t] = 1;
+          return;
+        }
+        const size_t off = (size_t)k * chunk, len = std::min(chunk, bytes - off);
+        std::memcpy(dst + off, stage + off, len);
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (char f : fail)
+    if (f) CK(cudaStreamSynchronize(c.stream));  // surfaces the CUDA error
+}
+
+static void run_body(Ctx& c, int32_t x_p, int64_t n_prefix, const int64_t* prefixes, int64_t branch_lo,
+                     int64_t branch_hi, double* out_host, void* out_device, int32_t accumulate, gs_stats* stats) {
+  const gs::Program& p = c.prog;
+  const int x = p.n_cross;
+  if (x_p < 0 || x_p > x) throw GsError(GS_ERR_PLAN, "x_p outside [0, x]");
+  if (n_prefix < 0 || (n_prefix > 0 && !prefixes)) throw GsError(GS_ERR_ARG, "bad prefix array");
+  // digit suffix products; spaces must fit int64
+  c.x_p = x_p;
+  c.S_p.assign(x_p + 1, 1);
+  for (int k = x_p - 1; k >= 0; --k) {
+    if (c.S_p[k + 1] > (1LL << 62) / p.radix[k]) throw GsError(GS_ERR_ARG, "prefix space exceeds 2^62");
+    c.S_p[k] = c.S_p[k + 1] * p.radix[k];
+  }
+  c.S_b.assign(x + 1, 1);
+  for (int k = x - 1; k >= x_p; --k) {
+    if (c.S_b[k + 1] > (1LL << 62) / p.radix[k]) throw GsError(GS_ERR_ARG, "branch space exceeds 2^62");
+    c.S_b[k] = c.S_b[k + 1] * p.radix[k];
+  }
+  const int64_t prefix_space = c.S_p[0], branch_space = c.S_b[x_p];
+  if (branch_lo < 0 || branch_hi > branch_space || branch_lo > branch_hi)
+    throw GsError(GS_ERR_ARG, "branch range outside the branch space");
+  c.prefixes.assign(prefixes, prefixes + n_prefix);
+  for (int64_t v : c.prefixes)
+    if (v < 0 || v >= prefix_space) throw GsError(GS_ERR_ARG, "prefix id outside the prefix space");
+  std::sort(c.prefixes.begin(), c.prefixes.end());
+  c.branch_lo = branch_lo;
+  c.branch_hi = branch_hi;
+  c.lvl_end.assign(p.levels.size(), 0);
+  for (size_t l = 1; l < p.levels.size(); ++l) c.lvl_end[l] = p.levels[l].k_hi;
+  c.st = gs_stats{};
+  const auto t_call = std::chrono::steady_clock::now();
+  c.last_tick = t_call;
+  if (!c.host_only) {
+    CK(cudaSetDevice(c.device));
+    if (!accumulate || !out_device) {
+      CK(cudaMemsetAsync(c.d_acc.p, 0, std::max<size_t>(c.n_req * sizeof(double2), 16), c.stream));
+    } else {
+      CK(cudaMemcpyAsync(c.d_acc.p, out_device, c.n_req * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream));
+    }
+    CK(cudaEventRecord(c.ev0, c.stream));
+  }
+  if (c.precision == GS_C64) gs::run_tree<float>(c);
+  else gs::run_tree<double>(c);
+  finish_requests(c);  // runs without a gather (no prefixes) still load the requests
+  c.st.host_ms_enqueue =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
+  static const bool prof = std::getenv("GS_HOST_PROF") != nullptr;
+  if (prof && c.st.host_ms_max_gap > 1.0)
+    std::fprintf(stderr, "gs_run host gap %.3f ms ending at '%s' (enqueue %.3f ms)\n", c.st.host_ms_max_gap,
+                 c.gap_label, c.st.host_ms_enqueue);
+  if (!c.host_only) {
+    CK(cudaEventRecord(c.ev1, c.stream));
+    if (out_device && c.n_req > 0)
+      CK(cudaMemcpyAsync(out_device, c.d_acc.p, c.n_req * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream));
+    if (out_host && c.n_req > 0) {
+      download_result(c, out_host);
+      c.st.d2h_bytes += 16.0 * c.n_req;
+    }
+    if (c.async_run && !out_host) {
+      c.st.ms_total = -1;  // still running: the caller orders on the stream
+    } else {
+      CK(cudaStreamSynchronize(c.stream));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+      c.st.ms_total = ms;
+    }
+  } else if (out_host) {
+    std::fill(out_host, out_host + 2 * std::max<int64_t>(c.n_req, 0), 0.0);
+  }
+  if (stats) *stats = c.st;
+}
+
+}  // namespace gs

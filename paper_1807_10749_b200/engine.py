@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "gs_run",
     "gs_describe",
     "gs_set_requests_global",
+    "gs_run_batched",
 )
 
 
@@ -97,6 +98,10 @@ def _load():
     lib.gs_set_requests.argtypes = [_P, ctypes.c_int64, _I64P, _I64P]
     lib.gs_set_requests_global.argtypes = [_P, ctypes.c_int64, _I64P, ctypes.c_int32, _I32P, _I32P]
     lib.gs_describe.argtypes = [_P, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+    lib.gs_run_batched.argtypes = [
+        _P, ctypes.c_int64, _I64P, ctypes.c_int32, _I32P, _I32P, ctypes.c_int32, ctypes.c_int64, _I64P,
+        ctypes.c_int64, ctypes.c_int64, _F64P, _P, ctypes.c_int32, ctypes.POINTER(GsStats),
+    ]
     lib.gs_run.argtypes = [
         _P, ctypes.c_int32, ctypes.c_int64, _I64P, ctypes.c_int64, ctypes.c_int64,
         _F64P, _P, ctypes.c_int32, ctypes.POINTER(GsStats),
@@ -257,6 +262,31 @@ class Engine:
         )
         self._requests = key
         self.n_req = int(a.size)
+
+    def run_batched(self, indices, n_qubits: int, block_a, block_b, x_p: int, prefixes, branch_lo: int,
+                    branch_hi: int, out: np.ndarray | None = None) -> RunResult:
+        """gs_run_batched: load `indices` (global basis indices) and sum the leaves
+        in one call; the request upload overlaps the first gate passes."""
+        idx = np.ascontiguousarray(indices, dtype=np.int64).ravel()
+        pidx = idx if idx.size else np.zeros(1, dtype=np.int64)
+        ba = np.ascontiguousarray(block_a, dtype=np.int32)
+        bb = np.ascontiguousarray(block_b, dtype=np.int32)
+        pre = np.ascontiguousarray(prefixes, dtype=np.int64).ravel()
+        ppre = pre if pre.size else np.zeros(1, dtype=np.int64)
+        # every entry is overwritten: no need to zero-fill
+        host = out if out is not None else np.empty(idx.size, dtype=np.complex128)
+        if host.dtype != np.complex128 or not host.flags.c_contiguous or host.size != idx.size:
+            raise ValueError("output must be a contiguous complex128 array with one entry per request")
+        hp = host.view(np.float64) if host.size else None
+        st = GsStats()
+        self.n_req = -1
+        self._requests = None
+        self._check(LIB.gs_run_batched(
+            self._h, idx.size, _ptr(pidx, ctypes.c_int64), int(n_qubits), _ptr(ba, ctypes.c_int32),
+            _ptr(bb, ctypes.c_int32), int(x_p), pre.size, _ptr(ppre, ctypes.c_int64), int(branch_lo),
+            int(branch_hi), _ptr(hp, ctypes.c_double) if hp is not None else None, None, 0, ctypes.byref(st)))
+        self.n_req = int(idx.size)
+        return RunResult(host, st.as_dict())
 
     def run(
         self,

@@ -48,10 +48,17 @@ def _engine_for(circuit: Circuit, plan: SimPlan, requests, device: int, dtype):
 
 
 def _run(circuit, plan, requests, prefixes, branch_lo, branch_hi, device, dtype):
-    eng, idx = _engine_for(circuit, plan, requests, device, dtype)
-    out = AmplitudeBatch.zeros(idx)
-    eng.run(plan.x_p, prefixes, branch_lo, branch_hi, out=out.amps)
-    return out
+    prog = lowered(circuit, plan.cut)
+    if prog.radices != tuple(int(r) for r in plan.radices):
+        raise ValueError("plan radices do not match the circuit's cross gates under plan.cut")
+    idx = np.asarray(requests, dtype=np.int64).ravel()
+    eng = ENGINES.get(device, dtype)
+    eng.load_program(prog)
+    # split_requests (pathsum.py:122-140) runs on the device, overlapped with the
+    # first gate passes; IndexError as in the reference
+    res = eng.run_batched(idx, circuit.n_qubits, plan.cut.block_a, plan.cut.block_b, plan.x_p, prefixes,
+                          branch_lo, branch_hi)
+    return AmplitudeBatch(idx, res.amps)
 
 
 def run_approx(

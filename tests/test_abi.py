@@ -132,3 +132,28 @@ def test_set_requests_global_validation():
         eng.set_requests_global(req, 15, plan.cut.block_a, plan.cut.block_b)
     with pytest.raises(ValueError):
         eng.set_requests_global(req, 16, plan.cut.block_a, plan.cut.block_a)
+
+
+def test_run_batched_host_only():
+    """gs_run_batched = set_requests_global + run: same tree, same validation."""
+    circ, plan, req, pre = configs.build("cfg1", n_req=64)
+    eng = host_engine()
+    eng.load_program(lowered(circ, plan.cut))
+    ba, bb = plan.cut.block_a, plan.cut.block_b
+    r = eng.run_batched(req, circ.n_qubits, ba, bb, plan.x_p, pre[:5], 0, plan.branch_space)
+    assert r.stats["n_paths"] == 5 * plan.branch_space
+    assert eng.n_req == req.size
+    # the requests stay loaded for plain runs
+    assert eng.run(plan.x_p, pre[:2], 0, plan.branch_space).stats["n_paths"] == 2 * plan.branch_space
+    bad = req.copy()
+    bad[-1] = 1 << circ.n_qubits
+    with pytest.raises(IndexError):
+        eng.run_batched(bad, circ.n_qubits, ba, bb, plan.x_p, pre[:5], 0, plan.branch_space)
+    with pytest.raises(RuntimeError):  # a failed call leaves no requests loaded
+        eng.run(plan.x_p, pre[:2], 0, plan.branch_space)
+    with pytest.raises(ValueError):
+        eng.run_batched(req, circ.n_qubits, ba, ba, plan.x_p, pre[:5], 0, plan.branch_space)
+    with pytest.raises(ValueError):  # bad prefix: workers joined, error reported
+        eng.run_batched(req, circ.n_qubits, ba, bb, plan.x_p, [plan.prefix_space], 0, plan.branch_space)
+    r = eng.run_batched(np.array([], dtype=np.int64), circ.n_qubits, ba, bb, plan.x_p, pre[:1], 0, 1)
+    assert r.amps.shape == (0,)

@@ -209,3 +209,24 @@ def test_async_run_stream_order(ps):
     for o, w in zip(outs, want):
         got = o.cpu().numpy().view(np.complex128)
         assert rel_l2(got, w) <= 1e-12
+
+
+def test_run_batched_call_matches_two_calls(ps):
+    """gs_run_batched (requests staged while the tree is enqueued) equals
+    gs_set_requests_global + gs_run, and a bad index raises before output."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build("cfg3", n_req=4096)
+    eng = _engine("c64")
+    eng.load_program(lowered(circ, plan.cut))
+    ba, bb = plan.cut.block_a, plan.cut.block_b
+    one = eng.run_batched(req, circ.n_qubits, ba, bb, plan.x_p, pre[:64], 0, plan.branch_space).amps.copy()
+    eng.set_requests_global(req, circ.n_qubits, ba, bb)
+    two = eng.run(plan.x_p, pre[:64], 0, plan.branch_space).amps
+    assert np.array_equal(one, two)
+    bad = req.copy()
+    bad[7] = -1
+    with pytest.raises(IndexError):
+        eng.run_batched(bad, circ.n_qubits, ba, bb, plan.x_p, pre[:64], 0, plan.branch_space)
+    again = eng.run_batched(req, circ.n_qubits, ba, bb, plan.x_p, pre[:64], 0, plan.branch_space).amps
+    assert np.array_equal(again, one)
