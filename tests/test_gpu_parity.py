@@ -230,3 +230,18 @@ def test_run_batched_call_matches_two_calls(ps):
         eng.run_batched(bad, circ.n_qubits, ba, bb, plan.x_p, pre[:64], 0, plan.branch_space)
     again = eng.run_batched(req, circ.n_qubits, ba, bb, plan.x_p, pre[:64], 0, plan.branch_space).amps
     assert np.array_equal(again, one)
+
+
+def test_pipelined_result_download(ps):
+    """d2h_chunk_mb > 0: chunked download through the pinned bounce buffer gives
+    the same host result as the direct copy."""
+    circ, plan, req, pre = configs.build("cfg3")
+    eng = _engine("c64")
+    want = ps.run_batched(circ, plan, req, prefixes=pre[:8]).amps
+    eng.set_option("d2h_chunk_mb", 1)
+    try:
+        got = ps.run_batched(circ, plan, req, prefixes=pre[:8]).amps
+    finally:
+        eng.set_option("d2h_chunk_mb", 0)
+    assert req.size * 16 > 3 * (1 << 20)
+    assert np.array_equal(got, want)
