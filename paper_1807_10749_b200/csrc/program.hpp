@@ -184,51 +184,86 @@ inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M, bool ve
   std::vector<int> last_fill;  // register bits of the latest stage no op needs
   bool first = true;
   while (!remaining.empty() || first) {
-    std::vector<char> in_r(k, 0);
-    int n_r = 0;
-    std::vector<char> blk_nd(k, 0), blk_d(k, 0);
-    std::vector<HostOp> taken, deferred;
     auto allowed = [&](int j) { return !first || hbm_ok(j); };
-    for (const HostOp& op : remaining) {
-      const int sb[2] = {op.s0, op.s1};
-      int tb[2] = {-1, -1};
-      for (int i = 0; i < 2; ++i)
-        if (sb[i] >= 0) tb[i] = tile_of[sb[i]];
-      bool nd_block = false, d_block = false;
-      for (int b : tb)
-        if (b >= 0) nd_block |= blk_nd[b], d_block |= blk_d[b];
-      if (op.diag()) {
-        if (nd_block) {
-          deferred.push_back(op);
-          for (int b : tb)
-            if (b >= 0) blk_d[b] = 1;
+    // ops a stage with register tile bits R can apply, in order: an op waits
+    // if it touches a bit of an earlier waiting op (diagonal ops commute with
+    // each other); a dense op also needs its bits in R
+    auto simulate = [&](uint32_t R, std::vector<HostOp>* taken, std::vector<HostOp>* deferred) {
+      uint32_t blk_nd = 0, blk_d = 0;
+      int n = 0;
+      for (const HostOp& op : remaining) {
+        uint32_t m = 0;
+        bool outside = false;
+        for (int sb : {op.s0, op.s1}) {
+          if (sb < 0) continue;
+          if (tile_of[sb] < 0) outside = true;
+          else m |= 1u << tile_of[sb];
+        }
+        const bool nd_block = (blk_nd & m) != 0, d_block = (blk_d & m) != 0;
+        bool take;
+        if (op.diag()) {
+          take = !nd_block;
+          if (!take) blk_d |= m;
         } else {
-          taken.push_back(op);
+          if (outside) throw GsError(-1, "dense op outside the tile: scheduler bug");
+          take = !nd_block && !d_block && (m & ~R) == 0;
+          if (!take) blk_nd |= m;
         }
-        continue;
-      }
-      bool ok = !(nd_block || d_block);
-      if (ok) {
-        int need = 0;
-        for (int i = 0; i < 2; ++i) {
-          if (sb[i] < 0) continue;
-          const int b = tb[i];
-          if (b < 0) { ok = false; break; }  // dense op outside the tile: scheduler bug
-          if (!in_r[b]) { ++need; if (!allowed(b)) ok = false; }
+        if (take) {
+          ++n;
+          if (taken) taken->push_back(op);
+        } else if (deferred) {
+          deferred->push_back(op);
         }
-        ok = ok && (n_r + need <= M);
       }
-      if (ok) {
-        for (int b : tb)
-          if (b >= 0 && !in_r[b]) in_r[b] = 1, ++n_r;
-        taken.push_back(op);
-      } else {
-        deferred.push_back(op);
-        for (int b : tb)
-          if (b >= 0) blk_nd[b] = 1;
+      return n;
+    };
+    // register set: the subset of the dense ops' (allowed) bits that lets this
+    // stage apply the most ops; among equals prefer one that finishes the pass
+    // with a store-compatible layout (no extra store stage)
+    uint32_t cand = 0;
+    for (const HostOp& op : remaining)
+      if (!op.diag())
+        for (int sb : {op.s0, op.s1})
+          if (sb >= 0 && tile_of[sb] >= 0 && allowed(tile_of[sb])) cand |= 1u << tile_of[sb];
+    std::vector<int> cbits;
+    for (int j = 0; j < k; ++j)
+      if ((cand >> j) & 1) cbits.push_back(j);
+    auto store_ok = [&](uint32_t R) {
+      if (group_log >= 3) return true;
+      for (int j = 0; j < k; ++j)
+        if (((R >> j) & 1) && !hbm_ok(j)) return false;
+      return true;
+    };
+    uint32_t best_R = cand;
+    if ((int)cbits.size() > M) {
+      int best_n = -1;
+      bool best_fin = false;
+      const int nc = (int)cbits.size();
+      for (uint32_t sel = (1u << M) - 1; sel < (1u << nc);) {
+        uint32_t R = 0;
+        for (int i = 0; i < nc; ++i)
+          if ((sel >> i) & 1) R |= 1u << cbits[i];
+        const int n = simulate(R, nullptr, nullptr);
+        const bool fin = n == (int)remaining.size() && store_ok(R);
+        if (n > best_n || (n == best_n && fin && !best_fin)) best_n = n, best_fin = fin, best_R = R;
+        const uint32_t lo = sel & -sel, r = sel + lo;  // next subset of the same size
+        sel = (((r ^ sel) >> 2) / lo) | r;
       }
     }
+    std::vector<HostOp> taken, deferred;
+    simulate(best_R, &taken, &deferred);
     if (taken.empty() && !first) throw GsError(-1, "stage scheduler made no progress");
+    // keep only the bits the taken dense ops use
+    uint32_t used = 0;
+    for (const HostOp& op : taken)
+      if (!op.diag())
+        for (int sb : {op.s0, op.s1})
+          if (sb >= 0) used |= 1u << tile_of[sb];
+    std::vector<char> in_r(k, 0);
+    int n_r = 0;
+    for (int j = 0; j < k; ++j)
+      if ((used >> j) & 1) in_r[j] = 1, ++n_r;
     if (vec && first && n_r < M && !in_r[0]) in_r[0] = 1, ++n_r;  // 16-byte loads
     std::vector<int> fill;
     for (int j = k - 1; j >= 0 && n_r < M; --j)

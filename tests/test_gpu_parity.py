@@ -243,5 +243,5 @@ def test_pipelined_result_download(ps):
         got = ps.run_batched(circ, plan, req, prefixes=pre[:8]).amps
     finally:
         eng.set_option("d2h_chunk_mb", 0)
-    assert req.size * 16 > 3 * (1 << 20)
+    assert req.size * 16 > (1 << 20)  # more than one chunk
     assert np.array_equal(got, want)
