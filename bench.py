@@ -334,7 +334,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (gate_pass_kernel) from the profiled step
+    # roofline of the dominant kernel (the specialised gate passes) from the profiled step
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -345,14 +345,26 @@ def main():
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
     ms_pass = prof["ms_pass"]
     launches = max(1, prof["n_pass_launches"])
+    traffic = None  # measured DRAM bytes per pass launch (ncu launch list committed under profiles/)
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(name)
+        if tr and args.window == 0:
+            traffic = tr["pass_dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {
         "bound": "hbm",
-        "kernel": "gate_pass_kernel",
+        "kernel": "gsj_* (load-time specialised gate passes)" if "jit:" in eng.describe()["jit"]
+                  else "pass2_kernel",
         "achieved": prof["pass_bytes_min"] / (ms_pass / 1e3) / 1e9 if ms_pass else None,
         "peak": peak,
         "unit": "GB/s",
         "frac": (prof["pass_bytes_min"] / (ms_pass / 1e3) / 1e9) / peak if ms_pass else None,
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_note": "DRAM read+write bytes per pass launch from profiles/traffic.json (ncu launch list "
+                        "of this config); below the algorithmic bytes where sibling nodes share their "
+                        "parent's tiles in L1/L2",
         "algorithmic_bytes_per_launch": prof["pass_bytes_min"] / launches,
         "avg_launch_ms": ms_pass / launches,
         "kernel_bytes_per_launch": prof["pass_bytes"] / launches,
