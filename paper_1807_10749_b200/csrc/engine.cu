@@ -223,6 +223,11 @@ struct Ctx {
   bool fused_active = false;  // the fused leaf pass is compiled for the loaded program
   bool bucket_valid = false;  // request buckets match the loaded requests
   DevBuf d_bcount, d_bstart, d_breq, d_btl, d_bia, d_cubtmp;
+  // requests sorted by A index for the HBM gathers (perm = original slot of sorted slot i)
+  int sort_requests = 1;   // option
+  int quad_gather = 1;     // option: 4 lanes per request in the grouped gather
+  bool req_sorted = false;
+  DevBuf d_ia_s, d_ib_s, d_perm, d_iota, d_sorttmp;
   int group_log = 3;  // leaves per group = 2^group_log (64-byte request reads in c64)
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
@@ -875,6 +880,7 @@ static void jit_program(Ctx& c) {
     const int n_chunks = std::max(1, std::min(m, std::min(hw, 32)));
     std::vector<std::string> src(n_chunks, jitgen::prelude());
     std::vector<std::vector<int>> members(n_chunks);
+    std::vector<std::vector<std::string>> names(n_chunks);
     std::vector<size_t> load(n_chunks, 0);
     std::vector<int> by_size(m);
     for (int i = 0; i < m; ++i) by_size[i] = i;
@@ -883,9 +889,12 @@ static void jit_program(Ctx& c) {
       const int ch = (int)(std::min_element(load.begin(), load.end()) - load.begin());
       const int local = (int)members[ch].size();
       // kernel text was generated as gsj_0: rename to its index inside the chunk
+      // plus the pass's global index (profiles map launches back to passes)
       std::string k = kernels[i];
       const size_t at = k.find("gsj_0(");
-      k.replace(at, 6, "gsj_" + std::to_string(local) + "(");
+      const std::string kname = "gsj_" + std::to_string(local) + "_p" + std::to_string(ids[i]);
+      k.replace(at, 6, kname + "(");
+      names[ch].push_back(kname);
       src[ch] += k;
       members[ch].push_back(i);
       load[ch] += k.size();
@@ -912,7 +921,7 @@ static void jit_program(Ctx& c) {
     for (int ch = 0; ch < n_chunks; ++ch)
       pool.emplace_back([&, ch] {
         cudaSetDevice(dev);
-        mods[ch] = jit_compile(src[ch], (int)members[ch].size(), "gridsim_passes_" + std::to_string(ch), errs[ch]);
+        mods[ch] = jit_compile(src[ch], names[ch], "gridsim_passes_" + std::to_string(ch), errs[ch]);
       });
     for (auto& t : pool) t.join();
     for (int ch = 0; ch < n_chunks; ++ch)
@@ -1263,6 +1272,36 @@ static void upload_weights(Ctx& c, const Node* nodes, int64_t n) {
   }
 }
 
+// Sort the split requests by their A index on stream `s` (radix sort of
+// (ia, slot) pairs + a gather of ib): the HBM gathers then read A runs in
+// ascending address order.  Results are unchanged -- every request's
+// partials are the same numbers, folded back to its slot by reduce_kernel.
+static void sort_requests(Ctx& c, cudaStream_t s) {
+  c.req_sorted = false;
+  const int64_t n = c.n_req;
+  if (c.host_only || !c.sort_requests || n < 1024 || n > INT32_MAX) return;
+  c.d_ia_s.ensure((size_t)n * 4);
+  c.d_ib_s.ensure((size_t)n * 4);
+  c.d_perm.ensure((size_t)n * 4);
+  c.d_iota.ensure((size_t)n * 4);
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  iota_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<int32_t*>(c.d_iota.p), n);
+  const uint32_t* kin = reinterpret_cast<const uint32_t*>(c.d_ia.p);
+  uint32_t* kout = reinterpret_cast<uint32_t*>(c.d_ia_s.p);
+  const int32_t* vin = reinterpret_cast<const int32_t*>(c.d_iota.p);
+  int32_t* vout = reinterpret_cast<int32_t*>(c.d_perm.p);
+  const int end_bit = std::max(1, c.prog.q[0]);
+  size_t tmp = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)n, 0, end_bit, s));
+  c.d_sorttmp.ensure(std::max<size_t>(tmp, 16));
+  CK(cub::DeviceRadixSort::SortPairs(c.d_sorttmp.p, tmp, kin, kout, vin, vout, (int)n, 0, end_bit, s));
+  permute_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const int32_t*>(c.d_ib.p), vout,
+                                        reinterpret_cast<int32_t*>(c.d_ib_s.p), n);
+  CK(cudaGetLastError());
+  c.req_sorted = true;
+  c.st.n_launches += 3;
+}
+
 // Complete the requests staged by gs_run_batched: join the host copies, then
 // upload + split on the side stream -- ordered after this run's start, so an
 // earlier queued run is done with the request buffers -- and make the run's
@@ -1284,6 +1323,7 @@ static void finish_requests(Ctx& c) {
       reinterpret_cast<const long long*>(c.d_gidx.p), n, c.pend.runs, reinterpret_cast<int32_t*>(c.d_ia.p),
       reinterpret_cast<int32_t*>(c.d_ib.p), c.pend.packed ? reinterpret_cast<uint32_t*>(c.d_packed.p) : nullptr);
   CK(cudaGetLastError());
+  sort_requests(c, c.side_stream);
   CK(cudaEventRecord(c.req_done, c.side_stream));
   CK(cudaStreamWaitEvent(c.stream, c.req_done, 0));
   c.st.h2d_bytes += 8.0 * n;
@@ -1307,7 +1347,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     const double2 kf = make_double2(ar * br - ai * bi, ar * bi + ai * br);
     reduce_kernel<<<(unsigned)xblocks, threads, 0, c.stream>>>(reinterpret_cast<const double2*>(c.d_partial.p),
                                                                 (int)groups, nreq, kf,
-                                                                reinterpret_cast<double2*>(c.d_acc.p));
+                                                                reinterpret_cast<double2*>(c.d_acc.p), nullptr);
     launch_check("reduce_kernel", xblocks, threads, 0);
     c.st.n_gather_launches += 1;
     c.st.n_launches += 1;
@@ -1327,6 +1367,16 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   c.d_partial.ensure((size_t)groups * nreq * sizeof(double2));
   const int qa = c.prog.q[0], qb = c.prog.q[1];
   const size_t pair_bytes = ((size_t)1 << qa) * c.esize() + ((size_t)1 << qb) * c.esize();
+  bool used_sorted = false;
+  const int32_t* g_ia = reinterpret_cast<const int32_t*>(c.d_ia.p);
+  const int32_t* g_ib = reinterpret_cast<const int32_t*>(c.d_ib.p);
+  const bool smem_path = !c.grouped_leaf && c.smem_gather && 2 * pair_bytes <= 200 * 1024 && qa + qb <= 31 &&
+                         qa >= 2 && qb >= 2;
+  if (c.req_sorted && !smem_path) {  // HBM gathers read A runs in ascending order
+    g_ia = reinterpret_cast<const int32_t*>(c.d_ia_s.p);
+    g_ib = reinterpret_cast<const int32_t*>(c.d_ib_s.p);
+    used_sorted = true;
+  }
   if (c.grouped_leaf) {
     const int GL = c.group_log;
     const int64_t ng = (n + (1 << GL) - 1) >> GL;
@@ -1336,14 +1386,18 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     const int64_t per_y = (ng + gy - 1) / gy;
     gy = (ng + per_y - 1) / per_y;
     c.d_partial.ensure((size_t)gy * nreq * sizeof(double2));
-    auto kern = GL == 3 ? gather_grouped_kernel<R, 3> : gather_grouped_kernel<R, 2>;
-    kern<<<dim3((unsigned)xblocks, (unsigned)gy), threads, 0, c.stream>>>(
+    auto kern = c.quad_gather
+                    ? (GL == 4 ? gather_grouped4_kernel<R, 4>
+                               : GL == 3 ? gather_grouped4_kernel<R, 3> : gather_grouped4_kernel<R, 2>)
+                    : (GL == 4 ? gather_grouped_kernel<R, 4>
+                               : GL == 3 ? gather_grouped_kernel<R, 3> : gather_grouped_kernel<R, 2>);
+    const int64_t gxb = c.quad_gather ? (4 * nreq + threads - 1) / threads : xblocks;
+    kern<<<dim3((unsigned)gxb, (unsigned)gy), threads, 0, c.stream>>>(
         c.leaf_out[0].p, c.leaf_out[1].p, 1LL << qa, 1LL << qb, (int)n, (int)per_y,
-        c.cur_weights, reinterpret_cast<const int32_t*>(c.d_ia.p),
-        reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
-    launch_check("gather_grouped_kernel", xblocks * gy, threads, 0);
+        c.cur_weights, g_ia, g_ib, nreq, reinterpret_cast<double2*>(c.d_partial.p));
+    launch_check("gather_grouped_kernel", gxb * gy, threads, 0);
     groups = gy;
-  } else if (c.smem_gather && 2 * pair_bytes <= 200 * 1024 && qa + qb <= 31 && qa >= 2 && qb >= 2) {
+  } else if (smem_path) {
     // shared-memory gather: whole leaf pairs staged per CTA, requests in registers
     constexpr int RPT = 20, NT = 512;
     const int64_t req_per_cta = (int64_t)RPT * NT;
@@ -1369,8 +1423,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   dim3 grid((unsigned)xblocks, (unsigned)groups);
   gather_kernel<R><<<grid, threads, 0, c.stream>>>(
       c.lvl_a[l].p, c.lvl_b[l].p, 1LL << qa, 1LL << qb, (int)n, (int)per,
-      c.cur_weights, reinterpret_cast<const int32_t*>(c.d_ia.p),
-      reinterpret_cast<const int32_t*>(c.d_ib.p), nreq, reinterpret_cast<double2*>(c.d_partial.p));
+      c.cur_weights, g_ia, g_ib, nreq, reinterpret_cast<double2*>(c.d_partial.p));
   launch_check("gather_kernel", xblocks * groups, threads, 0);
   }
   double2 kf = make_double2(1.0, 0.0);
@@ -1380,7 +1433,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   }
   reduce_kernel<<<(unsigned)xblocks, threads, 0, c.stream>>>(
       reinterpret_cast<const double2*>(c.d_partial.p), (int)groups, nreq, kf,
-      reinterpret_cast<double2*>(c.d_acc.p));
+      reinterpret_cast<double2*>(c.d_acc.p), used_sorted ? reinterpret_cast<const int32_t*>(c.d_perm.p) : nullptr);
   launch_check("reduce_kernel", xblocks, threads, 0);
   c.st.n_gather_launches += 2;
   c.st.n_launches += 2;
@@ -1686,6 +1739,10 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
         throw GsError(GS_ERR_ARG, "tile_bits out of range");
       c.tile_bits = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "quad_gather") {
+      c.quad_gather = value ? 1 : 0;
+    } else if (k == "sort_requests") {
+      c.sort_requests = value ? 1 : 0;
     } else if (k == "low_bits") {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "low_bits out of range");
       c.low_bits = (int)value;
@@ -1694,7 +1751,7 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       c.hoist = value ? 1 : 0;
       if (c.have_prog) throw GsError(GS_ERR_STATE, "set hoist before gs_load_program");
     } else if (k == "group_log") {
-      if (value != 2 && value != 3) throw GsError(GS_ERR_ARG, "group_log must be 2 or 3");
+      if (value < 2 || value > 4) throw GsError(GS_ERR_ARG, "group_log must be 2, 3 or 4");
       c.group_log = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "fuse_gather") {
@@ -1794,7 +1851,17 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
           }
           js += "], \"lbits\": [";
           for (size_t i = 0; i < pp.lbits.size(); ++i) js += (i ? ", " : "") + std::to_string(pp.lbits[i]);
-          js += "], \"grouped\": " + std::to_string(pp.grouped_store ? 1 : 0) + ", \"store_scale\": " + std::to_string(pp.store_scale) + "}";
+          js += "], \"grouped\": " + std::to_string(pp.grouped_store ? 1 : 0) + ", \"store_scale\": " + std::to_string(pp.store_scale) +
+                ", \"jit\": " + std::to_string(pp.jit_index) + ", \"opl\": \"";
+          for (const gs::HostOp& op : pp.ops) {
+            static const char kc[] = "dmDMx";
+            js += kc[op.kind < 5 ? op.kind : 4];
+            if (op.cross >= 0) js += "x";
+            js += std::to_string(op.s0);
+            if (op.s1 >= 0) js += ":" + std::to_string(op.s1);
+            js += " ";
+          }
+          js += "\"}";
         }
         js += "]}";
       }
@@ -1890,6 +1957,7 @@ int gs_set_requests_global(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32
     }
     c.n_req = n_req;
     c.bucket_valid = false;
+    gs::sort_requests(c, c.stream);
   });
 }
 
@@ -1976,6 +2044,7 @@ int gs_set_requests(gs_ctx* ctx, int64_t n_req, const int64_t* ia, const int64_t
     }
     c.n_req = n_req;
     c.bucket_valid = false;
+    gs::sort_requests(c, c.stream);
   });
 }
 

@@ -133,9 +133,10 @@ static std::string cache_path(const std::string& source) {
   return d + name;
 }
 
-static JitModule* load_cubin(const std::vector<char>& cubin, int n_kernels, std::string& err);
+static JitModule* load_cubin(const std::vector<char>& cubin, const std::vector<std::string>& names, std::string& err);
 
-JitModule* jit_compile(const std::string& source, int n_kernels, const std::string& tag, std::string& err) {
+JitModule* jit_compile(const std::string& source, const std::vector<std::string>& names, const std::string& tag,
+                       std::string& err) {
   if (!jit_available(err)) return nullptr;
   const std::string cpath = cache_path(source);
   if (!cpath.empty()) {
@@ -145,7 +146,7 @@ JitModule* jit_compile(const std::string& source, int n_kernels, const std::stri
       size_t r;
       while ((r = std::fread(buf, 1, sizeof buf, f)) > 0) cubin.insert(cubin.end(), buf, buf + r);
       std::fclose(f);
-      if (JitModule* m = load_cubin(cubin, n_kernels, err)) return m;
+      if (JitModule* m = load_cubin(cubin, names, err)) return m;
     }
   }
   NvrtcApi& n = nvrtc();
@@ -181,10 +182,11 @@ JitModule* jit_compile(const std::string& source, int n_kernels, const std::stri
       else std::remove(tmp.c_str());
     }
   }
-  return load_cubin(cubin, n_kernels, err);
+  return load_cubin(cubin, names, err);
 }
 
-static JitModule* load_cubin(const std::vector<char>& cubin, int n_kernels, std::string& err) {
+static JitModule* load_cubin(const std::vector<char>& cubin, const std::vector<std::string>& names, std::string& err) {
+  const int n_kernels = (int)names.size();
   DriverApi& d = driver();
   auto m = std::make_unique<JitModule>();
   CUresult cr = d.load(&m->mod, cubin.data());
@@ -195,7 +197,7 @@ static JitModule* load_cubin(const std::vector<char>& cubin, int n_kernels, std:
   m->fns.resize(n_kernels);
   m->smem_set.assign(n_kernels, 0);
   for (int i = 0; i < n_kernels; ++i) {
-    const std::string name = "gsj_" + std::to_string(i);
+    const std::string& name = names[i];
     cr = d.getfn(&m->fns[i], m->mod, name.c_str());
     if (cr != CUDA_SUCCESS) {
       err = "cuModuleGetFunction(" + name + ") failed";

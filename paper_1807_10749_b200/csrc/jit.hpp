@@ -45,8 +45,9 @@ struct JArgs {
 
 struct JitModule;
 
-// compile `source` (kernels gsj_0 .. gsj_{n-1}); returns nullptr with `err` set on failure
-JitModule* jit_compile(const std::string& source, int n_kernels, const std::string& tag, std::string& err);
+// compile `source` (extern "C" kernels `names`, looked up in that order); nullptr with `err` set on failure
+JitModule* jit_compile(const std::string& source, const std::vector<std::string>& names, const std::string& tag,
+                       std::string& err);
 void jit_release(JitModule* m);
 // thread-local memory (register spills) of kernel `idx`, bytes; -1 if unknown
 int jit_local_bytes(JitModule* m, int idx);

@@ -206,8 +206,11 @@ gather_kernel(const void* A, const void* B, long long a_elems, long long b_elems
   partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
 }
 
+// Fold the partials of request slot i into acc[perm ? perm[i] : i]: the
+// gathers may run over requests sorted by their A index (perm = the sort's
+// permutation), the accumulator stays in request order.
 static __global__ void __launch_bounds__(256)
-reduce_kernel(const double2* partial, int groups, long long n_req, double2 k, double2* acc) {
+reduce_kernel(const double2* partial, int groups, long long n_req, double2 k, double2* acc, const int32_t* perm) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_req) return;
   double2 s = make_double2(0.0, 0.0);
@@ -216,10 +219,11 @@ reduce_kernel(const double2* partial, int groups, long long n_req, double2 k, do
     s.x += p.x;
     s.y += p.y;
   }
-  double2 a = acc[i];
+  const long long o = perm ? (long long)perm[i] : i;
+  double2 a = acc[o];
   a.x += k.x * s.x - k.y * s.y;
   a.y += k.x * s.y + k.y * s.x;
-  acc[i] = a;
+  acc[o] = a;
 }
 
 }  // namespace gs
@@ -315,10 +319,16 @@ template <typename V, int W> struct Group { V v[W]; };
 
 template <typename V, int W> __device__ __forceinline__ Group<V, W> load_group(const V* p) {
   Group<V, W> q;
-  if constexpr (sizeof(V) == 8) {
+  if constexpr (sizeof(V) == 8 && W == 1) {
+    const float2 f = __ldg(reinterpret_cast<const float2*>(p));
+    q.v[0] = f;
+  } else if constexpr (sizeof(V) == 8) {
 #pragma unroll
     for (int k = 0; k < W / 2; ++k) {
-      const float4 f = __ldg(reinterpret_cast<const float4*>(p) + k);
+      float4 f;
+      asm volatile("ld.global.nc.L2::64B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w)
+                   : "l"(reinterpret_cast<const float4*>(p) + k));
       q.v[2 * k] = make_float2(f.x, f.y);
       q.v[2 * k + 1] = make_float2(f.z, f.w);
     }
@@ -358,6 +368,53 @@ gather_grouped_kernel(const void* A, const void* B, long long a_elems, long long
     }
   }
   partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
+}
+
+
+// Quad form of the grouped gather: 4 lanes per request, each reading a
+// 16-byte (complex64) / 32-byte (complex128) quarter of the request's 2^G-leaf
+// run, so one warp load covers 8 requests' whole runs (8 L1 wavefronts per
+// warp instruction instead of 32 -- the scattered thread-per-request loads
+// were L1-wavefront bound).  The four fp64 partial sums meet by shuffles.
+template <typename R, int GL>
+__global__ void __launch_bounds__(256)
+gather_grouped4_kernel(const void* A, const void* B, long long a_elems, long long b_elems, int n_leaves,
+                       int groups_per_y, const double* weights, const int32_t* ia, const int32_t* ib,
+                       long long n_req, double2* partial) {
+  using V = typename Cx<R>::T;
+  constexpr int W = 1 << GL;
+  constexpr int Q = W / 4;  // leaves per lane
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = t >> 2;
+  const int sub = (int)(t & 3);
+  const bool live = i < n_req;
+  const int n_groups = (n_leaves + W - 1) >> GL;
+  const int g0 = blockIdx.y * groups_per_y;
+  const int g1 = min(n_groups, g0 + groups_per_y);
+  const V* pa = reinterpret_cast<const V*>(A) + (live ? ((long long)ia[i] << GL) : 0) + sub * Q;
+  const V* pb = reinterpret_cast<const V*>(B) + (live ? ((long long)ib[i] << GL) : 0) + sub * Q;
+  double re = 0.0, im = 0.0;
+  if (live) {
+    for (int g = g0; g < g1; ++g) {
+      const Group<V, Q> x = load_group<V, Q>(pa + (((long long)g * a_elems) << GL));
+      const Group<V, Q> y = load_group<V, Q>(pb + (((long long)g * b_elems) << GL));
+#pragma unroll
+      for (int s = 0; s < Q; ++s) {
+        const int j = (g << GL) + sub * Q + s;
+        if (j < n_leaves) {
+          const double xr = x.v[s].x, xi = x.v[s].y, yr = y.v[s].x, yi = y.v[s].y;
+          const double w = weights[j];
+          re += w * (xr * yr - xi * yi);
+          im += w * (xr * yi + xi * yr);
+        }
+      }
+    }
+  }
+  re += __shfl_xor_sync(0xffffffffu, re, 1);
+  im += __shfl_xor_sync(0xffffffffu, im, 1);
+  re += __shfl_xor_sync(0xffffffffu, re, 2);
+  im += __shfl_xor_sync(0xffffffffu, im, 2);
+  if (live && sub == 0) partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
 }
 
 
@@ -406,6 +463,16 @@ static __device__ __forceinline__ void bucket_of(const BucketMap& m, unsigned ib
   tl = 0;
   for (int j = 0; j < m.n_g; ++j) tile |= ((ib >> m.gbits[j]) & 1u) << j;
   for (int j = 0; j < m.n_l; ++j) tl |= ((ib >> m.lbits[j]) & 1u) << j;
+}
+
+// request sort helpers (gather locality): v[i] = i; dst[i] = src[perm[i]]
+static __global__ void iota_kernel(int32_t* v, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+static __global__ void permute_kernel(const int32_t* src, const int32_t* perm, int32_t* dst, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[perm[i]];
 }
 
 static __global__ void bucket_count_kernel(const int32_t* ib, long long n, const BucketMap m, int32_t* count) {

@@ -245,3 +245,53 @@ def test_pipelined_result_download(ps):
         eng.set_option("d2h_chunk_mb", 0)
     assert req.size * 16 > (1 << 20)  # more than one chunk
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+def test_sorted_request_gather_is_bitwise_equal(ps, name):
+    """sort_requests=1 (the HBM gathers read requests sorted by A index, results
+    folded back to request order) gives exactly the unsorted sums, through all
+    three request-loading entry points."""
+    from paper_1807_10749_b200.lowering import lowered
+    from paper_1807_10749_b200.plan import split_requests
+
+    circ, plan, req, pre = configs.build(name, n_req=20000)
+    window = pre[:2] if name == "cfg5" else pre[:16]
+    branch_hi = 2 if name == "cfg5" else plan.branch_space
+    eng = _engine("c64")
+    eng.load_program(lowered(circ, plan.cut))
+    ba, bb = plan.cut.block_a, plan.cut.block_b
+    outs = {}
+    for srt in (0, 1):
+        eng.set_option("sort_requests", srt)
+        try:
+            a = eng.run_batched(req, circ.n_qubits, ba, bb, plan.x_p, window, 0, branch_hi).amps.copy()
+            eng.set_requests_global(req, circ.n_qubits, ba, bb)
+            b = eng.run(plan.x_p, window, 0, branch_hi).amps
+            ia, ib = split_requests(circ.n_qubits, ba, bb, req)
+            eng.set_requests(ia, ib)
+            c = eng.run(plan.x_p, window, 0, branch_hi).amps
+        finally:
+            eng.set_option("sort_requests", 1)
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+        outs[srt] = a
+    assert np.array_equal(outs[0], outs[1])
+    assert np.abs(outs[1]).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_quad_gather_matches_thread_per_request(ps, name):
+    """quad_gather=1 (4 lanes per request in the grouped gather, fp64 partials
+    joined by shuffles) agrees with one thread per request to fp64 rounding."""
+    g = load_amps(name)
+    circ, plan, _, _ = configs.build(name, n_req=4)
+    eng = _engine("c64")
+    got = {}
+    for q in (0, 1):
+        eng.set_option("quad_gather", q)
+        try:
+            got[q] = ps.run_batched(circ, plan, g["requests"], prefixes=g["prefixes"]).amps
+        finally:
+            eng.set_option("quad_gather", 1)
+    assert rel_l2(got[1], got[0]) <= 1e-13
+    assert rel_l2(got[1], g["amps_c64"]) <= C64_TOL
