@@ -169,6 +169,14 @@ int gs_run_batched(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32_t n_qub
                    const int64_t* prefixes, int64_t branch_lo, int64_t branch_hi, double* out_host,
                    void* out_device, int32_t accumulate, gs_stats* stats);
 
+/* Full state-vector simulation (reference run_full, statevec.py:410-446): the
+ * loaded program must be uncut -- n_qubits_b = 0, no cross gates, every op on
+ * block A (the whole register).  Evolves |0...0> through the same pass
+ * kernels and writes the 2^n_qubits_a amplitudes (qubit 0 = most significant
+ * bit; complex64 as (float re, float im) pairs in GS_C64 mode, complex128 as
+ * double pairs in GS_C128 mode) to out_host and/or out_device. */
+int gs_run_full(gs_ctx* ctx, void* out_host, void* out_device, gs_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -228,6 +228,7 @@ struct Ctx {
   int quad_gather = 1;     // option: 4 lanes per request in the grouped gather
   bool req_sorted = false;
   DevBuf d_ia_s, d_ib_s, d_perm, d_iota, d_sorttmp;
+  DevBuf full_state;  // gs_run_full
   int group_log = 3;  // leaves per group = 2^group_log (64-byte request reads in c64)
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
@@ -366,7 +367,9 @@ static void build_program(Ctx& c, int qa, int qb, int n_ops, const int32_t* kind
                           const int32_t* tkb, const int64_t* tcb, int64_t n_coef,
                           const double* coef) {
   Program p;
-  if (qa < 1 || qb < 1 || qa > 34 || qb > 34) throw GsError(GS_ERR_ARG, "block sizes out of range");
+  // qb = 0: an uncut full-state program (gs_run_full)
+  if (qa < 1 || qb < 0 || qa > 34 || qb > 34 || (qb == 0 && n_cross > 0))
+    throw GsError(GS_ERR_ARG, "block sizes out of range");
   p.q[0] = qa;
   p.q[1] = qb;
   p.coef.assign(coef, coef + 2 * n_coef);
@@ -655,6 +658,10 @@ static void schedule_program(Ctx& c) {
     Level& L = p.levels[l];
     for (int side = 0; side < 2; ++side) {
       const int kcap = ((int)l == D && c.grouped_leaf) ? c.kmax() - c.group_log : c.kmax();
+      if (p.q[side] == 0) {  // empty block of a full-state program
+        L.passes[side].clear();
+        continue;
+      }
       L.passes[side] = schedule_passes(L.ops[side], p.q[side], kcap, c.low_bits, true);
       if ((int)l == D && c.grouped_leaf) {
         L.passes[side].back().grouped_store = true;
@@ -2017,6 +2024,70 @@ int gs_run_batched(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32_t n_qub
   });
 }
 
+int gs_run_full(gs_ctx* ctx, void* out_host, void* out_device, gs_stats* stats) {
+  if (!ctx) return GS_ERR_ARG;
+  GS_GUARD(ctx, {
+    Ctx& c = ctx->c;
+    if (!c.have_prog) throw GsError(GS_ERR_STATE, "no program loaded");
+    if (c.prog.q[1] != 0 || c.prog.n_cross != 0 || c.prog.levels.size() != 1)
+      throw GsError(GS_ERR_ARG, "gs_run_full needs an uncut program (n_qubits_b = 0, no cross gates)");
+    c.st = gs_stats{};
+    const auto t_call = std::chrono::steady_clock::now();
+    c.last_tick = t_call;
+    const int q = c.prog.q[0];
+    const int64_t n = 1LL << q;
+    const size_t bytes = (size_t)n * c.esize();
+    if (!c.host_only) {
+      CK(cudaSetDevice(c.device));
+      c.full_state.ensure(bytes);
+      CK(cudaEventRecord(c.ev0, c.stream));
+    }
+    void* st = c.full_state.p;
+    {
+      gs::Timer t(c, &c.st.ms_pass);
+      bool first = true;
+      for (const gs::PassPlan& pp : c.prog.levels[0].passes[0]) {  // in place after the first pass
+        if (c.precision == GS_C64) {
+          if (c.kernel_version == 2 && pp.M > 0) gs::launch_pass2<float>(c, 0, pp, st, st, nullptr, nullptr, 1, first);
+          else gs::launch_pass<float>(c, 0, pp, st, st, nullptr, nullptr, 1, first);
+        } else {
+          if (c.kernel_version == 2 && pp.M > 0) gs::launch_pass2<double>(c, 0, pp, st, st, nullptr, nullptr, 1, first);
+          else gs::launch_pass<double>(c, 0, pp, st, st, nullptr, nullptr, 1, first);
+        }
+        first = false;
+      }
+      if (first) throw GsError(GS_ERR_ARG, "full-state program has no pass");
+    }
+    c.st.n_nodes = 1;
+    c.st.n_levels = 1;
+    c.st.pass_bytes_min = 2.0 * (double)bytes;
+    if (!c.host_only) {
+      const unsigned blocks = (unsigned)((n + 255) / 256);
+      if (c.precision == GS_C64)
+        gs::scale_state_kernel<float><<<blocks, 256, 0, c.stream>>>(st, n, c.kfinal[0][0], c.kfinal[0][1]);
+      else
+        gs::scale_state_kernel<double><<<blocks, 256, 0, c.stream>>>(st, n, c.kfinal[0][0], c.kfinal[0][1]);
+      CK(cudaGetLastError());
+      c.st.n_launches += 1;
+      CK(cudaEventRecord(c.ev1, c.stream));
+      if (out_device) CK(cudaMemcpyAsync(out_device, st, bytes, cudaMemcpyDeviceToDevice, c.stream));
+      if (out_host) {
+        CK(cudaMemcpyAsync(out_host, st, bytes, cudaMemcpyDeviceToHost, c.stream));
+        c.st.d2h_bytes += (double)bytes;
+      }
+      CK(cudaStreamSynchronize(c.stream));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+      c.st.ms_total = ms;
+    } else if (out_host) {
+      std::memset(out_host, 0, bytes);
+    }
+    c.st.host_ms_enqueue =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();
+    if (stats) *stats = c.st;
+  });
+}
+
 int gs_set_requests(gs_ctx* ctx, int64_t n_req, const int64_t* ia, const int64_t* ib) {
   if (!ctx) return GS_ERR_ARG;
   GS_GUARD(ctx, {
@@ -2112,6 +2183,7 @@ static void run_body(Ctx& c, int32_t x_p, int64_t n_prefix, const int64_t* prefi
                      int64_t branch_hi, double* out_host, void* out_device, int32_t accumulate, gs_stats* stats) {
   const gs::Program& p = c.prog;
   const int x = p.n_cross;
+  if (p.q[1] == 0) throw GsError(GS_ERR_STATE, "an uncut (full-state) program runs through gs_run_full");
   if (x_p < 0 || x_p > x) throw GsError(GS_ERR_PLAN, "x_p outside [0, x]");
   if (n_prefix < 0 || (n_prefix > 0 && !prefixes)) throw GsError(GS_ERR_ARG, "bad prefix array");
   // digit suffix products; spaces must fit int64

@@ -465,6 +465,21 @@ static __device__ __forceinline__ void bucket_of(const BucketMap& m, unsigned ib
   for (int j = 0; j < m.n_l; ++j) tl |= ((ib >> m.lbits[j]) & 1u) << j;
 }
 
+// state *= k (complex), in place: the deferred W-form scalar of a full-state run
+template <typename R>
+__global__ void scale_state_kernel(void* state, long long n, double kr, double ki) {
+  using V = typename Cx<R>::T;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V* p = reinterpret_cast<V*>(state);
+  const V v = p[i];
+  const R r = (R)kr, m = (R)ki;
+  V o;
+  o.x = v.x * r - v.y * m;
+  o.y = v.x * m + v.y * r;
+  p[i] = o;
+}
+
 // request sort helpers (gather locality): v[i] = i; dst[i] = src[perm[i]]
 static __global__ void iota_kernel(int32_t* v, long long n) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -106,6 +106,7 @@ def _load():
         _P, ctypes.c_int32, ctypes.c_int64, _I64P, ctypes.c_int64, ctypes.c_int64,
         _F64P, _P, ctypes.c_int32, ctypes.POINTER(GsStats),
     ]
+    lib.gs_run_full.argtypes = [_P, _P, _P, ctypes.POINTER(GsStats)]
     if lib.gs_abi_version() != 1:
         raise ImportError("libgridsim_b200.so ABI version mismatch")
     return lib
@@ -286,6 +287,21 @@ class Engine:
             _ptr(bb, ctypes.c_int32), int(x_p), pre.size, _ptr(ppre, ctypes.c_int64), int(branch_lo),
             int(branch_hi), _ptr(hp, ctypes.c_double) if hp is not None else None, None, 0, ctypes.byref(st)))
         self.n_req = int(idx.size)
+        return RunResult(host, st.as_dict())
+
+    def run_full(self, out: np.ndarray | None = None) -> RunResult:
+        """gs_run_full: the loaded (uncut) program's full state, complex64 (c64
+        engine) or complex128 (c128), qubit 0 in the most significant bit."""
+        prog = self._program
+        if prog is None:
+            raise RuntimeError("no program loaded")
+        dt = np.complex64 if self.precision == 0 else np.complex128
+        n = 1 << int(prog.n_a)
+        host = out if out is not None else np.empty(n, dtype=dt)
+        if host.dtype != dt or not host.flags.c_contiguous or host.size != n:
+            raise ValueError(f"output must be a contiguous {np.dtype(dt).name} array of 2^{prog.n_a} entries")
+        st = GsStats()
+        self._check(LIB.gs_run_full(self._h, host.ctypes.data_as(_P), None, ctypes.byref(st)))
         return RunResult(host, st.as_dict())
 
     def run(
