@@ -242,6 +242,11 @@ struct Ctx {
   std::string jit_status = "off";
   double jit_seconds = 0;
   std::vector<size_t> jit_smem;
+  std::vector<int> jit_occ;   // resident CTAs per SM of a pipelined (persistent) pass kernel
+  int pipeline = 0;           // option: persistent cp.async-prefetching pass kernels (JIT)
+  int dedupe_parent = 0;      // option: sibling slots load a shared parent tile once (JIT; measured slower)
+  int jit_cross_inline = 1;   // option: cross-term coefficients per digit as immediates (JIT)
+  int n_sm = 148;
   // requests
   int64_t n_req = -1;
   DevBuf d_ia, d_ib, d_acc, d_partial, d_gidx;
@@ -872,6 +877,8 @@ static void jit_program(Ctx& c) {
   }
   c.jit_smem.assign(n, 0);
   c.jit_loc.assign(n, {0, 0});
+  c.jit_occ.assign(n, 1);
+  for (PassPlan* pp : order) pp->pipelined = c.pipeline && !pp->fused_gather;
   // compile passes `ids` with a register bound for `min_blocks` CTAs/SM, in
   // chunks compiled concurrently (~source-size balanced, up to the core count)
   auto compile = [&](const std::vector<int>& ids, int min_blocks, std::string& err) -> bool {
@@ -879,7 +886,8 @@ static void jit_program(Ctx& c) {
     for (size_t t = 0; t < ids.size(); ++t) {
       PassPlan& pp = *order[ids[t]];
       size_t smem = 0;
-      kernels[t] = jitgen::pass_kernel(c, pp, 0, smem, pp.fused_gather, min_blocks);
+      kernels[t] = pp.pipelined ? jitgen::pass_kernel_pipe(c, pp, 0, smem)
+                                : jitgen::pass_kernel(c, pp, 0, smem, pp.fused_gather, min_blocks);
       c.jit_smem[ids[t]] = smem;
     }
     const int m = (int)ids.size();
@@ -968,6 +976,13 @@ static void jit_program(Ctx& c) {
       c.jit_status = err;
       return;
     }
+  }
+  for (int i = 0; i < n; ++i) {  // resident CTAs per SM of the persistent kernels
+    if (!order[i]->pipelined) continue;
+    const int regs = std::max(1, jit_num_regs(c.jit_mods[c.jit_loc[i].first], c.jit_loc[i].second));
+    const int by_regs = 65536 / (256 * ((regs + 7) / 8 * 8));
+    const int by_smem = (int)((228u << 10) / (c.jit_smem[i] + 1024));
+    c.jit_occ[i] = std::max(1, std::min(by_regs, by_smem));
   }
   c.jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   c.jit = c.jit_mods[0];
@@ -1201,7 +1216,12 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
     std::string err;
     const size_t jsm = c.jit_smem[pp.jit_index];
     const auto loc = c.jit_loc[pp.jit_index];
-    if (jit_launch(c.jit_mods[loc.first], loc.second, (unsigned)blocks, threads, jsm, c.stream, j, err) !=
+    int64_t grid = blocks;
+    if (pp.pipelined) {  // persistent: the CTAs loop over the tiles
+      j.n_ctas = blocks;
+      grid = std::min<int64_t>(blocks, (int64_t)c.n_sm * c.jit_occ[pp.jit_index]);
+    }
+    if (jit_launch(c.jit_mods[loc.first], loc.second, (unsigned)grid, threads, jsm, c.stream, j, err) !=
         cudaSuccess)
       throw GsError(GS_ERR_CUDA, "jit pass launch: " + err);
     return;
@@ -1687,6 +1707,7 @@ int gs_create(int device, int precision, gs_ctx** out) {
   }
   try {
     CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&h->c.n_sm, cudaDevAttrMultiProcessorCount, device));
     CK(cudaStreamCreateWithFlags(&h->c.own_stream, cudaStreamNonBlocking));
     h->c.stream = h->c.own_stream;
     CK(cudaEventCreate(&h->c.ev0));
@@ -1745,6 +1766,15 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (value != 0 && (value < 4 || value > (c.precision == GS_C64 ? 14 : 13)))
         throw GsError(GS_ERR_ARG, "tile_bits out of range");
       c.tile_bits = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "jit_cross_inline") {
+      c.jit_cross_inline = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "dedupe_parent") {
+      c.dedupe_parent = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pipeline") {
+      c.pipeline = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "quad_gather") {
       c.quad_gather = value ? 1 : 0;

@@ -214,6 +214,12 @@ int jit_local_bytes(JitModule* m, int idx) {
   return v;
 }
 
+int jit_num_regs(JitModule* m, int idx) {
+  int v = 0;
+  if (driver().getattr(&v, CU_FUNC_ATTRIBUTE_NUM_REGS, m->fns[idx]) != CUDA_SUCCESS) return -1;
+  return v;
+}
+
 void jit_release(JitModule* m) {
   if (!m) return;
   if (m->mod && driver().ok) driver().unload(m->mod);

@@ -41,6 +41,7 @@ struct JArgs {
   void* partial;              // double2 [leaf group][n_req]
   long long n_req;
   long long a_elems;
+  long long n_ctas;   // logical tiles of a persistent (pipelined) pass kernel
 };
 
 struct JitModule;
@@ -51,6 +52,8 @@ JitModule* jit_compile(const std::string& source, const std::vector<std::string>
 void jit_release(JitModule* m);
 // thread-local memory (register spills) of kernel `idx`, bytes; -1 if unknown
 int jit_local_bytes(JitModule* m, int idx);
+// registers per thread of kernel `idx`; -1 if unknown
+int jit_num_regs(JitModule* m, int idx);
 // launch kernel `idx` of the module
 cudaError_t jit_launch(JitModule* m, int idx, unsigned grid, unsigned block, size_t smem, cudaStream_t s,
                        const JArgs& args, std::string& err);

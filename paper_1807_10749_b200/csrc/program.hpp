@@ -62,6 +62,7 @@ struct PassPlan {
   int jit_index = -1;           // kernel gsj_<index> of the program's JIT module
   bool grouped_store = false;   // leaf level, last pass: grouped path-minor store
   bool fused_gather = false;    // leaf level, last B pass: gather instead of a B store (JIT)
+  bool pipelined = false;       // JIT: persistent kernel prefetching the next tile (option pipeline)
 };
 
 struct Level {

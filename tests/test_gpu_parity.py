@@ -295,3 +295,49 @@ def test_quad_gather_matches_thread_per_request(ps, name):
             eng.set_option("quad_gather", 1)
     assert rel_l2(got[1], got[0]) <= 1e-13
     assert rel_l2(got[1], g["amps_c64"]) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg2h", "cfg3", "cfg4", "cfg5"])
+def test_pipelined_pass_kernels_bitwise(ps, name):
+    """pipeline=1 (persistent pass kernels prefetching the next tile with
+    cp.async) runs the same arithmetic: bitwise equal sums."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    window = pre[:2] if name == "cfg5" else pre[:8]
+    branch_hi = 2 if name == "cfg5" else plan.branch_space
+    eng = _engine("c64")
+    got = {}
+    for pipe in (0, 1):
+        eng.set_option("pipeline", pipe)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[pipe] = eng.run(plan.x_p, window, 0, branch_hi).amps
+        finally:
+            eng.set_option("pipeline", 0)
+    assert np.array_equal(got[0], got[1])
+    assert np.abs(got[1]).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2h", "cfg3", "cfg4"])
+def test_parent_dedupe_bitwise(ps, name):
+    """dedupe_parent=1 (sibling slots load their shared parent tile once, via
+    shared memory) computes bitwise the same sums as every slot loading it."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    eng = _engine("c64")
+    got = {}
+    for d in (0, 1):
+        eng.set_option("dedupe_parent", d)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            # an odd branch range: sibling groups that do not share a parent too
+            got[d] = (eng.run(plan.x_p, pre[:12], 0, plan.branch_space).amps,
+                      eng.run(plan.x_p, pre[:5], 1, plan.branch_space - 1).amps)
+        finally:
+            eng.set_option("dedupe_parent", 1)
+    for a, b in zip(got[0], got[1]):
+        assert np.array_equal(a, b) and np.abs(a).max() > 0
