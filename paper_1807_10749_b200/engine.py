@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "gs_describe",
     "gs_set_requests_global",
     "gs_run_batched",
+    "gs_run_full",
 )
 
 
