@@ -246,6 +246,10 @@ struct Ctx {
   int pipeline = 0;           // option: persistent cp.async-prefetching pass kernels (JIT)
   int dedupe_parent = 0;      // option: sibling slots load a shared parent tile once (JIT; measured slower)
   int jit_cross_inline = 1;   // option: cross-term coefficients per digit as immediates (JIT)
+  int tail_gather = 1;        // option: small last leaf pass evaluated inside the (path-major) gather
+  int tail_max = 3;           // option: max tail qubits (2^tail_max reads per request and leaf)
+  std::vector<HostOp> tail_ops[2];
+  std::vector<int> tail_bits[2];
   int n_sm = 148;
   // requests
   int64_t n_req = -1;
@@ -644,6 +648,39 @@ static void emit_prims(Ctx& c, int side, const Level& L, const HostOp& op, const
 
 static uint64_t pack_level_digits(const Program& p, int l, int64_t v);
 
+// the leaves are gathered by the path-major gather_kernel (not the grouped or
+// shared-memory layouts)
+static bool plain_gather(const Ctx& c) {
+  const Program& p = c.prog;
+  const size_t pair_bytes = (((size_t)1 << p.q[0]) + ((size_t)1 << p.q[1])) * c.esize();
+  const bool smem_ok = c.smem_gather && 2 * pair_bytes <= 200 * 1024 && p.q[0] + p.q[1] <= 31 && p.q[0] >= 2 &&
+                       p.q[1] >= 2;
+  return !c.grouped_leaf && !smem_ok;
+}
+
+// A leaf side's last pass whose ops are one-/two-qubit gates on at most
+// tail_max qubits (plus diagonal gates anywhere, no cross terms) is not run:
+// the gather applies it per request (gather_tail_kernel).
+static void extract_tail(Ctx& c, Level& L, int side) {
+  c.tail_ops[side].clear();
+  c.tail_bits[side].clear();
+  if (!c.tail_gather || c.kernel_version != 2 || c.prog.q[1] == 0 || !plain_gather(c) || L.passes[side].size() < 2)
+    return;  // (a full-state program has no gather)
+  const PassPlan& last = L.passes[side].back();
+  if (last.ops.empty() || last.ops.size() > 16) return;
+  std::vector<int> T;
+  for (const HostOp& op : last.ops) {
+    if (op.cross >= 0) return;
+    if (op.diag()) continue;
+    for (int b : {op.s0, op.s1})
+      if (b >= 0 && std::find(T.begin(), T.end(), b) == T.end()) T.push_back(b);
+  }
+  if ((int)T.size() > c.tail_max || T.empty()) return;
+  c.tail_ops[side] = last.ops;
+  c.tail_bits[side] = T;
+  L.passes[side].pop_back();
+}
+
 static void schedule_program(Ctx& c) {
   Program& p = c.prog;
   ++c.sched_serial;
@@ -668,6 +705,7 @@ static void schedule_program(Ctx& c) {
         continue;
       }
       L.passes[side] = schedule_passes(L.ops[side], p.q[side], kcap, c.low_bits, true);
+      if ((int)l == D) extract_tail(c, L, side);
       if ((int)l == D && c.grouped_leaf) {
         L.passes[side].back().grouped_store = true;
         if (side == 1 && c.fuse_gather && c.group_log == 3 && c.precision == GS_C64)
@@ -1010,6 +1048,30 @@ static void upload_program(Ctx& c) {
     upload(c, c.d_params, f);
   } else {
     upload(c, c.d_params, c.host_params);
+  }
+  {  // leaf tails evaluated in the gather
+    TailProgD tp[2];
+    std::memset(tp, 0, sizeof tp);
+    for (int side = 0; side < 2; ++side) {
+      const auto& T = c.tail_bits[side];
+      tp[side].t = (int)T.size();
+      for (size_t k = 0; k < T.size(); ++k) tp[side].tb[k] = T[k];
+      tp[side].n_ops = (int)c.tail_ops[side].size();
+      for (size_t o = 0; o < c.tail_ops[side].size(); ++o) {
+        const HostOp& op = c.tail_ops[side][o];
+        TailOpD& d = tp[side].ops[o];
+        auto kidx = [&](int b) {
+          const auto it = std::find(T.begin(), T.end(), b);
+          return it == T.end() ? -1 : (int)(it - T.begin());
+        };
+        d.kind = op.kind == K_MAT1 ? 0 : op.kind == K_DIAG1 ? 1 : op.kind == K_DIAG2 ? 2 : 3;
+        d.s0 = op.s0, d.s1 = op.s1;
+        d.k0 = kidx(op.s0), d.k1 = op.s1 >= 0 ? kidx(op.s1) : -1;
+        const int64_t n = coef_entries(op.kind);
+        for (int64_t e = 0; e < 2 * n; ++e) d.u[e] = c.prog.coef[2 * op.coef + e];
+      }
+    }
+    CK(cudaMemcpyToSymbol(g_tail, tp, sizeof tp));
   }
   upload(c, c.d_xtable, c.prog.xtable);
   if (c.precision == GS_C64) {
@@ -1446,6 +1508,26 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
         nreq, (int)req_per_cta, reinterpret_cast<double2*>(c.d_partial.p));
     launch_check("gather_smem_kernel", xb * g, NT, 2 * pair_bytes);
     groups = g;
+  } else if (!c.tail_ops[0].empty() || !c.tail_ops[1].empty()) {
+    dim3 grid((unsigned)xblocks, (unsigned)groups);
+    const int ta = (int)c.tail_bits[0].size(), tb = (int)c.tail_bits[1].size();
+    const void* A = c.lvl_a[l].p;
+    const void* B = c.lvl_b[l].p;
+#define GS_TAIL(TA, TB)                                                                                     \
+  case TA * 4 + TB:                                                                                         \
+    gather_tail_kernel<R, TA, TB><<<grid, threads, 0, c.stream>>>(A, B, 1LL << qa, 1LL << qb, (int)n, (int)per, \
+                                                                  c.cur_weights, g_ia, g_ib, nreq,           \
+                                                                  reinterpret_cast<double2*>(c.d_partial.p)); \
+    break;
+    switch (ta * 4 + tb) {
+      GS_TAIL(0, 0) GS_TAIL(0, 1) GS_TAIL(0, 2) GS_TAIL(0, 3)
+      GS_TAIL(1, 0) GS_TAIL(1, 1) GS_TAIL(1, 2) GS_TAIL(1, 3)
+      GS_TAIL(2, 0) GS_TAIL(2, 1) GS_TAIL(2, 2) GS_TAIL(2, 3)
+      GS_TAIL(3, 0) GS_TAIL(3, 1) GS_TAIL(3, 2) GS_TAIL(3, 3)
+      default: throw GsError(GS_ERR_ARG, "leaf tail wider than 3 qubits");
+    }
+#undef GS_TAIL
+    launch_check("gather_tail_kernel", xblocks * groups, threads, 0);
   } else {
   dim3 grid((unsigned)xblocks, (unsigned)groups);
   gather_kernel<R><<<grid, threads, 0, c.stream>>>(
@@ -1767,6 +1849,13 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
         throw GsError(GS_ERR_ARG, "tile_bits out of range");
       c.tile_bits = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "tail_gather") {
+      c.tail_gather = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "tail_max") {
+      if (value < 1 || value > 3) throw GsError(GS_ERR_ARG, "tail_max must be 1..3");
+      c.tail_max = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "jit_cross_inline") {
       c.jit_cross_inline = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -1904,7 +1993,8 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
       }
       js += "]}";
     }
-    js += "], \"jit\": \"";
+    js += "], \"tail\": [" + std::to_string(c.tail_ops[0].size()) + ", " + std::to_string(c.tail_ops[1].size()) +
+          "], \"jit\": \"";
     for (char ch : c.jit_status) js += (ch == '"' || ch == '\\' || ch == '\n') ? ' ' : ch;
     js += "\"}";
     if (needed) *needed = (int64_t)js.size() + 1;

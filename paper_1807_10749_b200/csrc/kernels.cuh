@@ -206,6 +206,163 @@ gather_kernel(const void* A, const void* B, long long a_elems, long long b_elems
   partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
 }
 
+// ---------------------------------------------------------------------------
+// Leaf tails in the gather.  When the last pass of a leaf side only applies
+// one-qubit gates on a few qubits T (|T| <= 3) plus diagonal gates (cfg5: the
+// final H layer on the qubits the tile had no room for), that pass is not run;
+// the gather evaluates it per request instead: the 2^|T| stored amplitudes
+// around the requested index, the tail ops on that small vector (fp64), then
+// the requested entry -- 2^|T| sector reads per request instead of a full
+// read + write of the 2 GiB half-state per leaf.
+
+struct TailOpD {
+  int kind;    // 0 mat1 (k0), 1 diag1, 2 diag2, 3 mat2 (k0, k1)
+  int k0, k1;  // index of the op's bit in T, or -1 (diag ops on bits outside T)
+  int s0, s1;  // state bits
+  int pad[3];
+  double u[32];  // complex coefficients: mat1 4, diag1 2, diag2 4, mat2 16
+};
+struct TailProgD {
+  int n_ops, t, pad[2];
+  int tb[4];  // state bit of tail index bit k
+  TailOpD ops[16];
+};
+__constant__ TailProgD g_tail[2];
+
+template <int T> __device__ __forceinline__ int tail_bit(long long x, int j, int k, int s) {
+  return k >= 0 ? ((j >> k) & 1) : (int)((x >> s) & 1);
+}
+
+template <int T, int K>
+__device__ __forceinline__ void tail_m1(double* vr, double* vi, const double* u) {
+#pragma unroll
+  for (int j = 0; j < (1 << T); ++j) {
+    if ((j >> K) & 1) continue;
+    const int f = j | (1 << K);
+    const double ar = vr[j], ai = vi[j], br = vr[f], bi = vi[f];
+    vr[j] = u[0] * ar - u[1] * ai + u[2] * br - u[3] * bi;
+    vi[j] = u[0] * ai + u[1] * ar + u[2] * bi + u[3] * br;
+    vr[f] = u[4] * ar - u[5] * ai + u[6] * br - u[7] * bi;
+    vi[f] = u[4] * ai + u[5] * ar + u[6] * bi + u[7] * br;
+  }
+}
+
+template <int T, int K0, int K1>
+__device__ __forceinline__ void tail_m2(double* vr, double* vi, const double* u) {
+#pragma unroll
+  for (int j = 0; j < (1 << T); ++j) {
+    if (((j >> K0) & 1) || ((j >> K1) & 1)) continue;
+    double xr[4], xi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int id = j | ((q >> 1) << K0) | ((q & 1) << K1);
+      xr[q] = vr[id];
+      xi[q] = vi[id];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double ur = u[2 * (4 * r + q)], ui = u[2 * (4 * r + q) + 1];
+        sr += ur * xr[q] - ui * xi[q];
+        si += ur * xi[q] + ui * xr[q];
+      }
+      const int id = j | ((r >> 1) << K0) | ((r & 1) << K1);
+      vr[id] = sr;
+      vi[id] = si;
+    }
+  }
+}
+
+template <typename R, int T>
+__device__ __forceinline__ double2 tail_amp(const typename Cx<R>::T* st, long long x, int side) {
+  using V = typename Cx<R>::T;
+  if constexpr (T == 0) {
+    const V v = st[x];
+    return make_double2((double)v.x, (double)v.y);
+  } else {
+    constexpr int N = 1 << T;
+    const TailProgD& tp = g_tail[side];
+    long long x0 = x;
+#pragma unroll
+    for (int k = 0; k < T; ++k) x0 &= ~(1LL << tp.tb[k]);
+    double vr[N], vi[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      long long y = x0;
+#pragma unroll
+      for (int k = 0; k < T; ++k)
+        if ((j >> k) & 1) y |= 1LL << tp.tb[k];
+      const V v = st[y];
+      vr[j] = v.x;
+      vi[j] = v.y;
+    }
+    for (int o = 0; o < tp.n_ops; ++o) {
+      const TailOpD& op = tp.ops[o];
+      const double* u = op.u;
+      if (op.kind == 0) {  // dense 2x2 on tail bit k0 (static register indices per case)
+        switch (op.k0) {
+          case 0: tail_m1<T, 0>(vr, vi, u); break;
+          case 1: if constexpr (T > 1) tail_m1<T, 1>(vr, vi, u); break;
+          default: if constexpr (T > 2) tail_m1<T, 2>(vr, vi, u); break;
+        }
+      } else if (op.kind == 3) {  // dense 4x4 on tail bits (k0, k1), |s0 s1> order
+        if constexpr (T > 1) {
+          switch (op.k0 * 4 + op.k1) {
+            case 1: tail_m2<T, 0, 1>(vr, vi, u); break;
+            case 4: tail_m2<T, 1, 0>(vr, vi, u); break;
+            case 2: if constexpr (T > 2) tail_m2<T, 0, 2>(vr, vi, u); break;
+            case 8: if constexpr (T > 2) tail_m2<T, 2, 0>(vr, vi, u); break;
+            case 6: if constexpr (T > 2) tail_m2<T, 1, 2>(vr, vi, u); break;
+            default: if constexpr (T > 2) tail_m2<T, 2, 1>(vr, vi, u); break;
+          }
+        }
+      } else {  // diagonal: entry by the element's bits (tail bits or bits of x)
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          int d = tail_bit<T>(x, j, op.k0, op.s0);
+          if (op.kind == 2) d = 2 * d + tail_bit<T>(x, j, op.k1, op.s1);
+          const double dr = u[2 * d], di = u[2 * d + 1];
+          const double ar = vr[j], ai = vi[j];
+          vr[j] = dr * ar - di * ai;
+          vi[j] = dr * ai + di * ar;
+        }
+      }
+    }
+    int jx = 0;
+#pragma unroll
+    for (int k = 0; k < T; ++k) jx |= (int)((x >> tp.tb[k]) & 1) << k;
+    double rr = 0.0, ri = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (j == jx) rr = vr[j], ri = vi[j];
+    return make_double2(rr, ri);
+  }
+}
+
+template <typename R, int TA, int TB>
+__global__ void __launch_bounds__(256)
+gather_tail_kernel(const void* A, const void* B, long long a_elems, long long b_elems, int n_leaves,
+                   int leaves_per_group, const double* weights, const int32_t* ia, const int32_t* ib,
+                   long long n_req, double2* partial) {
+  using V = typename Cx<R>::T;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_req) return;
+  const int j0 = blockIdx.y * leaves_per_group;
+  const int j1 = min(n_leaves, j0 + leaves_per_group);
+  const long long xa = ia[i], xb = ib[i];
+  double re = 0.0, im = 0.0;
+  for (int j = j0; j < j1; ++j) {
+    const double2 x = tail_amp<R, TA>(reinterpret_cast<const V*>(A) + (long long)j * a_elems, xa, 0);
+    const double2 y = tail_amp<R, TB>(reinterpret_cast<const V*>(B) + (long long)j * b_elems, xb, 1);
+    const double w = weights[j];
+    re += w * (x.x * y.x - x.y * y.y);
+    im += w * (x.x * y.y + x.y * y.x);
+  }
+  partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
+}
+
 // Fold the partials of request slot i into acc[perm ? perm[i] : i]: the
 // gathers may run over requests sorted by their A index (perm = the sort's
 // permutation), the accumulator stays in request order.

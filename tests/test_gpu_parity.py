@@ -341,3 +341,43 @@ def test_parent_dedupe_bitwise(ps, name):
             eng.set_option("dedupe_parent", 1)
     for a, b in zip(got[0], got[1]):
         assert np.array_equal(a, b) and np.abs(a).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg5f"])
+def test_tail_gather_matches_tail_pass(ps, name):
+    """tail_gather=1 (the leaf's small last pass evaluated per request inside
+    the gather, fp64) agrees with running that pass (fp32) to rounding."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    eng = _engine("c64")
+    got = {}
+    for t in (0, 1):
+        eng.set_option("tail_gather", t)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            if t:
+                assert sum(eng.describe()["tail"]) > 0
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[t] = eng.run(plan.x_p, pre[:1], 0, 2).amps
+        finally:
+            eng.set_option("tail_gather", 1)
+    assert rel_l2(got[1], got[0]) <= 1e-6
+
+
+@pytest.mark.parametrize("case", SMALL)
+def test_tail_gather_small_cases(ps, case):
+    """Small circuits forced onto the path-major gather with 5-qubit tiles (multi-pass
+    leaf levels, tails of 1-3 qubits incl. diagonal ops on outside bits) vs the reference."""
+    circ, plan, req, g = small_case(case)
+    eng = _engine("c64")
+    opts = {"smem_gather": 0, "grouped_leaf": 0, "tile_bits": 5}
+    try:
+        for k, v in opts.items():
+            eng.set_option(k, v)
+        got = ps.run_approx(circ, plan, req).amps
+    finally:
+        eng.set_option("smem_gather", 1)
+        eng.set_option("grouped_leaf", 1)
+        eng.set_option("tile_bits", 0)
+    assert rel_l2(got, g["amps_c64"]) <= C64_TOL
