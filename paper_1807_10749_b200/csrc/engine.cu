@@ -246,6 +246,7 @@ struct Ctx {
   int pipeline = 0;           // option: persistent cp.async-prefetching pass kernels (JIT)
   int dedupe_parent = 0;      // option: sibling slots load a shared parent tile once (JIT; measured slower)
   int jit_cross_inline = 1;   // option: cross-term coefficients per digit as immediates (JIT)
+  int jit_spill_ok = 32;      // option: local-memory bytes tolerated at the 3-CTA register bound
   int tail_gather = 1;        // option: small last leaf pass evaluated inside the (path-major) gather
   int tail_max = 3;           // option: max tail qubits (2^tail_max reads per request and leaf)
   std::vector<HostOp> tail_ops[2];
@@ -1006,7 +1007,7 @@ static void jit_program(Ctx& c) {
   if (c.jit_min_blocks > 0) {
     std::vector<int> spill;
     for (int i = 0; i < n; ++i)
-      if (jit_local_bytes(c.jit_mods[c.jit_loc[i].first], c.jit_loc[i].second) > 0) spill.push_back(i);
+      if (jit_local_bytes(c.jit_mods[c.jit_loc[i].first], c.jit_loc[i].second) > c.jit_spill_ok) spill.push_back(i);
     n_spill = (int)spill.size();
     if (!spill.empty() && !compile(spill, 0, err)) {
       for (JitModule* md : c.jit_mods) jit_release(md);
@@ -1849,6 +1850,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
         throw GsError(GS_ERR_ARG, "tile_bits out of range");
       c.tile_bits = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "jit_spill_ok") {
+      c.jit_spill_ok = (int)std::max<int64_t>(0, value);
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "tail_gather") {
       c.tail_gather = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -1857,7 +1861,8 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       c.tail_max = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "jit_cross_inline") {
-      c.jit_cross_inline = value ? 1 : 0;
+      if (value < 0 || value > 3) throw GsError(GS_ERR_ARG, "jit_cross_inline must be 0..3");
+      c.jit_cross_inline = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "dedupe_parent") {
       c.dedupe_parent = value ? 1 : 0;
