@@ -369,7 +369,10 @@ def main():
         "traffic": traffic,
         "traffic_note": "DRAM read+write bytes per pass launch from profiles/traffic.json (ncu launch list "
                         "of this config); below the algorithmic bytes where sibling nodes share their "
-                        "parent's tiles in L1/L2",
+                        "parent's tiles in L1/L2 (the algorithmic count reads the parent once per child, so "
+                        "frac can exceed 1; dram_frac is the measured-DRAM fraction)",
+        "dram_achieved": (traffic / (ms_pass / launches / 1e3) / 1e9) if (traffic and ms_pass) else None,
+        "dram_frac": (traffic / (ms_pass / launches / 1e3) / 1e9 / peak) if (traffic and ms_pass) else None,
         "algorithmic_bytes_per_launch": prof["pass_bytes_min"] / launches,
         "avg_launch_ms": ms_pass / launches,
         "kernel_bytes_per_launch": prof["pass_bytes"] / launches,

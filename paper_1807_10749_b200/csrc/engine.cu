@@ -247,6 +247,8 @@ struct Ctx {
   int dedupe_parent = 0;      // option: sibling slots load a shared parent tile once (JIT; measured slower)
   int jit_cross_inline = 1;   // option: cross-term coefficients per digit as immediates (JIT)
   int jit_spill_ok = 32;      // option: local-memory bytes tolerated at the 3-CTA register bound
+  int uniform_chunks = 0;     // option: full fan-out chunks derive parent/digits from the slot (JIT; no measured gain)
+  int64_t uni_p0 = -1;        // current chunk: parent slot of its first node when full fan-out
   int tail_gather = 1;        // option: small last leaf pass evaluated inside the (path-major) gather
   int tail_max = 3;           // option: max tail qubits (2^tail_max reads per request and leaf)
   std::vector<HostOp> tail_ops[2];
@@ -706,6 +708,7 @@ static void schedule_program(Ctx& c) {
         continue;
       }
       L.passes[side] = schedule_passes(L.ops[side], p.q[side], kcap, c.low_bits, true);
+      for (PassPlan& pp : L.passes[side]) pp.level = (int)l;
       if ((int)l == D) extract_tail(c, L, side);
       if ((int)l == D && c.grouped_leaf) {
         L.passes[side].back().grouped_store = true;
@@ -1265,6 +1268,7 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
     j.state_elems = 1LL << q;
     j.n_states = n_states;
     j.init_zero = init_zero ? 1 : 0;
+    j.uni_p0 = c.uni_p0;
     if (pp.fused_gather) {
       j.aleaf = c.leaf_out[0].p;
       j.ia = reinterpret_cast<const int32_t*>(c.d_bia.p);  // A index per bucket slot
@@ -1582,8 +1586,19 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
       c.st.h2d_bytes += 12.0 * n;
     }
     if (l + 1 == D) upload_weights(c, chunk, n);  // the fused leaf pass reads them
+    // full fan-out chunk: node j is child j % F of parent chunk[0].parent + j / F
+    c.uni_p0 = -1;
+    if (c.uniform_chunks) {
+      const int64_t F = level_fanout(c.prog, l + 1);
+      bool uni = F >= 1 && F <= 65536;
+      for (int64_t j = 0; uni && j < n; ++j)
+        uni = chunk[j].parent == chunk[0].parent + j / F &&
+              chunk[j].digit == pack_level_digits(c.prog, l + 1, j % F);
+      if (uni) c.uni_p0 = chunk[0].parent;
+    }
     run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
                         at(c.lvl_b, l + 1), d_parent, d_digit, false);
+    c.uni_p0 = -1;
     descend<R>(c, l + 1, chunk, n);
   }
 }
@@ -1850,6 +1865,8 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
         throw GsError(GS_ERR_ARG, "tile_bits out of range");
       c.tile_bits = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "uniform_chunks") {
+      c.uniform_chunks = value ? 1 : 0;
     } else if (k == "jit_spill_ok") {
       c.jit_spill_ok = (int)std::max<int64_t>(0, value);
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }

@@ -42,6 +42,7 @@ struct JArgs {
   long long n_req;
   long long a_elems;
   long long n_ctas;   // logical tiles of a persistent (pipelined) pass kernel
+  long long uni_p0;   // >= 0: the chunk is full fan-out -- parent = uni_p0 + slot / F, digits from slot % F
 };
 
 struct JitModule;

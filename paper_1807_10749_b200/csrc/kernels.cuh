@@ -552,17 +552,29 @@ gather_grouped4_kernel(const void* A, const void* B, long long a_elems, long lon
   const V* pb = reinterpret_cast<const V*>(B) + (live ? ((long long)ib[i] << GL) : 0) + sub * Q;
   double re = 0.0, im = 0.0;
   if (live) {
-    for (int g = g0; g < g1; ++g) {
-      const Group<V, Q> x = load_group<V, Q>(pa + (((long long)g * a_elems) << GL));
-      const Group<V, Q> y = load_group<V, Q>(pb + (((long long)g * b_elems) << GL));
+    // U groups' loads in flight per lane before any is consumed (the loop was
+    // one DRAM round trip per group: latency-bound at ~4 TB/s)
+    constexpr int U = 4;
+    for (int g = g0; g < g1; g += U) {
+      Group<V, Q> x[U], y[U];
 #pragma unroll
-      for (int s = 0; s < Q; ++s) {
-        const int j = (g << GL) + sub * Q + s;
-        if (j < n_leaves) {
-          const double xr = x.v[s].x, xi = x.v[s].y, yr = y.v[s].x, yi = y.v[s].y;
-          const double w = weights[j];
-          re += w * (xr * yr - xi * yi);
-          im += w * (xr * yi + xi * yr);
+      for (int u = 0; u < U; ++u) {
+        const int gg = min(g + u, g1 - 1);
+        x[u] = load_group<V, Q>(pa + (((long long)gg * a_elems) << GL));
+        y[u] = load_group<V, Q>(pb + (((long long)gg * b_elems) << GL));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (g + u >= g1) break;
+#pragma unroll
+        for (int s = 0; s < Q; ++s) {
+          const int j = ((g + u) << GL) + sub * Q + s;
+          if (j < n_leaves) {
+            const double xr = x[u].v[s].x, xi = x[u].v[s].y, yr = y[u].v[s].x, yi = y[u].v[s].y;
+            const double w = weights[j];
+            re += w * (xr * yr - xi * yi);
+            im += w * (xr * yi + xi * yr);
+          }
         }
       }
     }

@@ -63,6 +63,7 @@ struct PassPlan {
   bool grouped_store = false;   // leaf level, last pass: grouped path-minor store
   bool fused_gather = false;    // leaf level, last B pass: gather instead of a B store (JIT)
   bool pipelined = false;       // JIT: persistent kernel prefetching the next tile (option pipeline)
+  int level = -1;               // path-tree level of the pass
 };
 
 struct Level {

@@ -381,3 +381,26 @@ def test_tail_gather_small_cases(ps, case):
         eng.set_option("grouped_leaf", 1)
         eng.set_option("tile_bits", 0)
     assert rel_l2(got, g["amps_c64"]) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2h", "cfg3", "cfg4", "cfg5"])
+def test_uniform_chunks_bitwise(ps, name):
+    """uniform_chunks=1 (full fan-out chunks compute parent/digits from the slot)
+    gives bitwise the node-table results, incl. partial branch ranges."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    window = pre[:2] if name == "cfg5" else pre[:9]
+    eng = _engine("c64")
+    got = {}
+    for u in (0, 1):
+        eng.set_option("uniform_chunks", u)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[u] = (eng.run(plan.x_p, window, 0, plan.branch_space).amps,
+                      eng.run(plan.x_p, window, 1, plan.branch_space - 1).amps)
+        finally:
+            eng.set_option("uniform_chunks", 1)
+    for a, b in zip(got[0], got[1]):
+        assert np.array_equal(a, b) and np.abs(a).max() > 0
