@@ -770,8 +770,9 @@ static void schedule_program(Ctx& c) {
         // tile = k state bits + slot bits batching small states, up to 2^13 (c64) /
         // 2^12 (c128) amplitudes and 256 threads
         pp.K = std::max(pp.k, std::min(c.kmax(), pp.M + 8));
+        if (pp.grouped_store) pp.K = pp.k + c.group_log;  // the grouped store interleaves 2^G slots
         // complex64 specialised passes use 16-byte HBM accesses (jitgen.inc)
-        const bool vec = c.precision == GS_C64 && c.use_jit && c.vec_hbm && pp.M == 5;
+        const bool vec = c.precision == GS_C64 && c.use_jit && c.vec_hbm && (pp.M == 5 || pp.M == 4);
         pp.stages = schedule_stages(pp, pp.M, vec, pp.grouped_store ? c.group_log : 0);
         pp.dev_stage_offset = (int64_t)c.host_pstages.size();
         pp.goff_offset = (int64_t)c.host_gofftab.size();
@@ -911,7 +912,7 @@ static void jit_program(Ctx& c) {
   for (Level& L : c.prog.levels)
     for (int side = 0; side < 2; ++side)
       for (PassPlan& pp : L.passes[side])
-        if (pp.M == 5 && !pp.stages.empty()) order.push_back(&pp);
+        if ((pp.M == 5 || pp.M == 4) && !pp.stages.empty()) order.push_back(&pp);
   const int n = (int)order.size();
   if (n == 0) {
     c.jit_status = "no eligible passes";

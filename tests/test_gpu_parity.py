@@ -404,3 +404,20 @@ def test_uniform_chunks_bitwise(ps, name):
             eng.set_option("uniform_chunks", 1)
     for a, b in zip(got[0], got[1]):
         assert np.array_equal(a, b) and np.abs(a).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg2h", "cfg3", "cfg4"])
+def test_four_register_bit_passes(ps, name):
+    """reg_bits=4 (512-thread CTAs, 16 amplitudes per thread, specialised too)
+    matches the reference windows."""
+    g = load_amps(name)
+    circ, plan, _, _ = configs.build(name, n_req=4)
+    eng = _engine("c64")
+    eng.set_option("reg_bits", 4)
+    eng.set_option("jit_min_blocks", 2)
+    try:
+        got = ps.run_batched(circ, plan, g["requests"], prefixes=g["prefixes"]).amps
+    finally:
+        eng.set_option("reg_bits", 5)
+        eng.set_option("jit_min_blocks", 3)
+    assert rel_l2(got, g["amps_c64"]) <= C64_TOL
