@@ -232,7 +232,8 @@ struct Ctx {
   int group_log = 3;  // leaves per group = 2^group_log (64-byte request reads in c64)
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
-  int reg_bits = 5;  // register bits per stage for c64 (4 or 5)
+  int reg_bits = 5;  // register bits per stage for c64 (4 or 5; 0 = per pass by op count)
+  int m4_ops = 30;   // reg_bits = 0: passes with at least this many ops use 4 register bits
   int use_jit = 1;   // specialise passes at load time (NVRTC); interpreter otherwise
   int vec_hbm = 1;   // option: vector (16-byte) HBM stage layouts for specialised passes
   int jit_min_blocks = 3;  // option: __launch_bounds__ min CTAs/SM of specialised passes (0 = none)
@@ -765,7 +766,11 @@ static void schedule_program(Ctx& c) {
       for (PassPlan& pp : L.passes[side]) {
         // register bits per stage: 5 (c64) / 4 (c128); tiny states (< 4 qubits in
         // the tile) keep the v1 shared-memory kernel
-        pp.M = (c.precision == GS_C64 && pp.k >= 5 && c.reg_bits != 4) ? 5 : (pp.k >= 4 ? 4 : 0);
+        // 5 register bits (256 threads) by default; 4 (512 threads, 2 CTAs/SM) for
+        // the op-heavy, non-grouped passes when reg_bits = 0 (auto, m4_ops threshold)
+        bool m4 = c.reg_bits == 4;
+        if (c.reg_bits == 0) m4 = c.use_jit && !pp.grouped_store && (int)pp.ops.size() >= c.m4_ops;
+        pp.M = (c.precision == GS_C64 && pp.k >= 5 && !m4) ? 5 : (pp.k >= 4 ? 4 : 0);
         if (pp.M == 0) continue;
         // tile = k state bits + slot bits batching small states, up to 2^13 (c64) /
         // 2^12 (c128) amplitudes and 256 threads
@@ -930,7 +935,8 @@ static void jit_program(Ctx& c) {
       PassPlan& pp = *order[ids[t]];
       size_t smem = 0;
       kernels[t] = pp.pipelined ? jitgen::pass_kernel_pipe(c, pp, 0, smem)
-                                : jitgen::pass_kernel(c, pp, 0, smem, pp.fused_gather, min_blocks);
+                                : jitgen::pass_kernel(c, pp, 0, smem, pp.fused_gather,
+                                                      pp.M == 4 && min_blocks > 2 ? 2 : min_blocks);
       c.jit_smem[ids[t]] = smem;
     }
     const int m = (int)ids.size();
@@ -1926,8 +1932,11 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "jit") {
       c.use_jit = value ? 1 : 0;  // the HBM stage layout depends on it: reschedule
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "m4_ops") {
+      c.m4_ops = (int)std::max<int64_t>(1, value);
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "reg_bits") {
-      if (value != 4 && value != 5) throw GsError(GS_ERR_ARG, "reg_bits must be 4 or 5");
+      if (value != 0 && value != 4 && value != 5) throw GsError(GS_ERR_ARG, "reg_bits must be 0, 4 or 5");
       c.reg_bits = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pass_kernel") {
