@@ -254,6 +254,15 @@ struct Ctx {
   int tail_max = 3;           // option: max tail qubits (2^tail_max reads per request and leaf)
   std::vector<HostOp> tail_ops[2];
   std::vector<int> tail_bits[2];
+  int proj_leaf = 1;          // option: a projector-only leaf side is read from its parent in the gather
+  int proj_perm = 0;          // option: store those parents with the sibling-run bits lowest (no measured gain)
+  int proj_side = -1;         // leaf side evaluated by projection (no leaf passes), -1 none
+  const int32_t* cur_parent = nullptr;             // device node tables of the current leaf chunk
+  const int32_t* cur_gpar = nullptr;               // per leaf group: shared parent of a sibling block, or -1
+  bool proj_fast = false;                          // run gates radix 2 with v(d) = d
+  std::vector<std::pair<int, int>> proj_swaps;     // parent states stored with these address-bit swaps
+  PassPlan* proj_perm_pass = nullptr;              // the pass that stores them permuted
+  const unsigned long long* cur_digit = nullptr;
   int n_sm = 148;
   // requests
   int64_t n_req = -1;
@@ -685,6 +694,34 @@ static void extract_tail(Ctx& c, Level& L, int side) {
   L.passes[side].pop_back();
 }
 
+// Leaf side whose cross terms are all projectors (one nonzero diagonal entry
+// per term: P0/P1 of a CZ cut) and whose other leaf ops are one-qubit gates
+// on those cross qubits only: its leaves are projections of the parent state
+// followed by a product of 2x2 gates (gather_proj_kernel), so no leaf pass runs.
+static bool projectable(const Ctx& c, int side) {
+  const Program& p = c.prog;
+  const int D = (int)p.levels.size() - 1;
+  if (D < 1 || p.q[1 - side] == 0) return false;
+  const Level& L = p.levels[D];
+  if (L.k_hi - L.k_lo > 8 || L.k_hi <= L.k_lo) return false;
+  std::vector<int> C;
+  for (int k = L.k_lo; k < L.k_hi; ++k) {
+    if (!p.xdiag[side][k] || p.radix[k] > 16) return false;
+    for (int d = 0; d < p.radix[k]; ++d) {
+      const double* x = &p.coef[2 * (size_t)p.xtable[p.xtab[side][k] + d]];
+      const bool n0 = x[0] != 0.0 || x[1] != 0.0, n1 = x[2] != 0.0 || x[3] != 0.0;
+      if (n0 == n1) return false;
+    }
+    C.push_back(p.q[side] - 1 - p.xq[side][k]);
+  }
+  for (const HostOp& op : L.ops[side]) {
+    if (op.cross >= 0) continue;
+    if (op.kind != K_MAT1 && op.kind != K_DIAG1) return false;
+    if (std::find(C.begin(), C.end(), op.s0) == C.end()) return false;
+  }
+  return true;
+}
+
 static void schedule_program(Ctx& c) {
   Program& p = c.prog;
   ++c.sched_serial;
@@ -700,9 +737,17 @@ static void schedule_program(Ctx& c) {
                      std::min(p.q[0], p.q[1]) >= 12 && std::max(p.q[0], p.q[1]) <= 24;
   }
   const int D = (int)p.levels.size() - 1;
+  c.proj_side = -1;
+  if (c.proj_leaf && c.grouped_leaf && !c.fuse_gather && c.kernel_version == 2)
+    for (int side = 0; side < 2 && c.proj_side < 0; ++side)
+      if (projectable(c, side)) c.proj_side = side;
   for (size_t l = 0; l < p.levels.size(); ++l) {
     Level& L = p.levels[l];
     for (int side = 0; side < 2; ++side) {
+      if ((int)l == D && side == c.proj_side) {  // leaves read from the parent in the gather
+        L.passes[side].clear();
+        continue;
+      }
       const int kcap = ((int)l == D && c.grouped_leaf) ? c.kmax() - c.group_log : c.kmax();
       if (p.q[side] == 0) {  // empty block of a full-state program
         L.passes[side].clear();
@@ -868,6 +913,39 @@ static void schedule_program(Ctx& c) {
     }
     c.kfinal[side][0] = kre;
     c.kfinal[side][1] = kim;
+  }
+  // projected leaf side: store its parents (the last pass of level D-1) with the
+  // run gates' qubits at address bits 0..G-1, so a sibling block's 2^G parent
+  // amplitudes are one contiguous run for the gather
+  c.proj_swaps.clear();
+  c.proj_perm_pass = nullptr;
+  if (c.proj_perm && c.proj_side >= 0 && D >= 2 && c.precision == GS_C64 && c.use_jit && !c.pipeline) {
+    const int ps = c.proj_side, q = p.q[ps];
+    Level& LP = p.levels[D - 1];
+    const Level& LD = p.levels[D];
+    const int nk = LD.k_hi - LD.k_lo;
+    if (!LP.passes[ps].empty() && nk >= c.group_log) {
+      PassPlan& last = LP.passes[ps].back();
+      std::vector<int> pos(q), inv(q);
+      for (int b = 0; b < q; ++b) pos[b] = inv[b] = b;
+      std::vector<std::pair<int, int>> sw;
+      for (int b = 0; b < c.group_log; ++b) {
+        const int sbit = q - 1 - p.xq[ps][LD.k_lo + nk - 1 - b];
+        const int cur = pos[sbit];
+        if (cur == b) continue;
+        const int other = inv[b];
+        pos[sbit] = b, pos[other] = cur, inv[b] = sbit, inv[cur] = other;
+        sw.push_back({cur, b});
+      }
+      bool ok = (last.M == 5 || last.M == 4) && !last.grouped_store && !sw.empty();
+      for (int b = 0; b < q && ok; ++b)
+        if (pos[b] != b) ok = std::find(last.lbits.begin(), last.lbits.end(), b) != last.lbits.end();
+      if (ok) {
+        last.store_perm = pos;
+        c.proj_swaps = sw;
+        c.proj_perm_pass = &last;
+      }
+    }
   }
   // packed-digit lookup per level (fan-outs up to 2^16)
   for (size_t l = 1; l < p.levels.size(); ++l) {
@@ -1084,6 +1162,7 @@ static void upload_program(Ctx& c) {
     }
     CK(cudaMemcpyToSymbol(g_tail, tp, sizeof tp));
   }
+
   upload(c, c.d_xtable, c.prog.xtable);
   if (c.precision == GS_C64) {
     std::vector<float> f(c.prog.coef.begin(), c.prog.coef.end());
@@ -1092,6 +1171,79 @@ static void upload_program(Ctx& c) {
     upload(c, c.d_coef, c.prog.coef);
   }
   jit_program(c);
+  {  // projected leaf side
+    ProjProgD pj;
+    std::memset(&pj, 0, sizeof pj);
+    pj.side = std::max(0, c.proj_side);
+    if (c.proj_side >= 0) {
+      const Program& p = c.prog;
+      const int side = c.proj_side;
+      const Level& L = p.levels.back();
+      pj.n = L.k_hi - L.k_lo;
+      for (int k = L.k_lo; k < L.k_hi; ++k) {
+        const int j = k - L.k_lo;
+        const int sb = p.q[side] - 1 - p.xq[side][k];
+        pj.s[j] = sb;
+        for (int d = 0; d < p.radix[k]; ++d) {
+          const double* x = &p.coef[2 * (size_t)p.xtable[p.xtab[side][k] + d]];
+          const int v = (x[2] != 0.0 || x[3] != 0.0) ? 1 : 0;
+          pj.v[j][d] = v;
+          pj.a[j][d][0] = x[2 * v];
+          pj.a[j][d][1] = x[2 * v + 1];
+        }
+        double U[8] = {1, 0, 0, 0, 0, 0, 1, 0};  // U <- u * U for the qubit's ops in order
+        for (const HostOp& op : L.ops[side]) {
+          if (op.cross >= 0 || op.s0 != sb) continue;
+          const double* cf = &p.coef[2 * (size_t)op.coef];
+          double u[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          if (op.kind == K_MAT1) {
+            for (int e = 0; e < 8; ++e) u[e] = cf[e];
+          } else {  // diag1
+            u[0] = cf[0], u[1] = cf[1], u[6] = cf[2], u[7] = cf[3];
+          }
+          double r[8];
+          for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) {
+              double re = 0, im = 0;
+              for (int m = 0; m < 2; ++m) {
+                const double ur = u[2 * (2 * a + m)], ui = u[2 * (2 * a + m) + 1];
+                const double vr = U[2 * (2 * m + b)], vi = U[2 * (2 * m + b) + 1];
+                re += ur * vr - ui * vi;
+                im += ur * vi + ui * vr;
+              }
+              r[2 * (2 * a + b)] = re, r[2 * (2 * a + b) + 1] = im;
+            }
+          std::memcpy(U, r, sizeof U);
+        }
+        std::memcpy(pj.u[j], U, sizeof U);
+      }
+    }
+    // the permuted parent layout needs the specialised kernel of that pass
+    if (c.proj_perm_pass && c.proj_perm_pass->jit_index < 0) {
+      c.proj_perm_pass->store_perm.clear();
+      c.proj_swaps.clear();
+      c.proj_perm_pass = nullptr;
+    }
+    pj.n_swap = (int)c.proj_swaps.size();
+    for (size_t k = 0; k < c.proj_swaps.size() && k < 4; ++k) pj.sa[k] = c.proj_swaps[k].first, pj.sb[k] = c.proj_swaps[k].second;
+    for (int k = 0; k < pj.n && k < 8; ++k) {  // address bit of each cross qubit (swaps applied)
+      int b = pj.s[k];
+      for (int w = 0; w < pj.n_swap; ++w)
+        if (b == pj.sa[w]) b = pj.sb[w];
+        else if (b == pj.sb[w]) b = pj.sa[w];
+      pj.abit[k] = b;
+    }
+    c.proj_fast = false;
+    if (c.proj_side >= 0 && pj.n >= c.group_log) {
+      const Level& L = c.prog.levels.back();
+      c.proj_fast = true;
+      for (int b = 0; b < c.group_log; ++b) {
+        const int j = pj.n - 1 - b;
+        c.proj_fast = c.proj_fast && c.prog.radix[L.k_lo + j] == 2 && pj.v[j][0] == 0 && pj.v[j][1] == 1;
+      }
+    }
+    CK(cudaMemcpyToSymbol(g_proj, &pj, sizeof pj));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1487,6 +1639,18 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     const int64_t per_y = (ng + gy - 1) / gy;
     gy = (ng + per_y - 1) / per_y;
     c.d_partial.ensure((size_t)gy * nreq * sizeof(double2));
+    if (c.proj_side >= 0) {  // one side's leaves come from its parent state
+      const int ps = c.proj_side;
+      const void* P = (ps == 0 ? c.lvl_a : c.lvl_b)[l - 1].p;
+      auto pk = GL == 4 ? gather_proj_kernel<R, 4> : GL == 3 ? gather_proj_kernel<R, 3> : gather_proj_kernel<R, 2>;
+      const int64_t gxb = (4 * nreq + threads - 1) / threads;
+      pk<<<dim3((unsigned)gxb, (unsigned)gy), threads, 0, c.stream>>>(
+          P, c.leaf_out[1 - ps].p, 1LL << c.prog.q[ps], 1LL << c.prog.q[1 - ps], (int)n, (int)per_y,
+          c.cur_weights, c.cur_parent, c.cur_digit, c.cur_gpar, g_ia, g_ib, nreq,
+          reinterpret_cast<double2*>(c.d_partial.p));
+      launch_check("gather_proj_kernel", gxb * gy, threads, 0);
+      groups = gy;
+    } else {
     auto kern = c.quad_gather
                     ? (GL == 4 ? gather_grouped4_kernel<R, 4>
                                : GL == 3 ? gather_grouped4_kernel<R, 3> : gather_grouped4_kernel<R, 2>)
@@ -1498,6 +1662,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
         c.cur_weights, g_ia, g_ib, nreq, reinterpret_cast<double2*>(c.d_partial.p));
     launch_check("gather_grouped_kernel", gxb * gy, threads, 0);
     groups = gy;
+    }
   } else if (smem_path) {
     // shared-memory gather: whole leaf pairs staged per CTA, requests in registers
     constexpr int RPT = 20, NT = 512;
@@ -1572,7 +1737,10 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
   c.tick("before enumerate");
   enumerate_children(c, l, nodes, n_nodes, kids);
   c.tick("enumerate_children");
-  const int64_t cap = c.cap[l + 1];
+  int64_t cap = c.cap[l + 1];
+  // leaf chunks of whole leaf groups: sibling blocks stay aligned with the
+  // grouped layout's 2^G-leaf groups across chunk boundaries
+  if (l + 1 == D && c.grouped_leaf && cap >= (1 << c.group_log)) cap -= cap % (1 << c.group_log);
   auto at = [](std::vector<DevBuf>& v, int i) -> void* { return i < (int)v.size() ? v[i].p : nullptr; };
   for (int64_t s = 0; s < (int64_t)kids.size(); s += cap) {
     const int64_t n = std::min<int64_t>(cap, (int64_t)kids.size() - s);
@@ -1592,7 +1760,43 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
       d_parent = reinterpret_cast<const int32_t*>(d_digit + n);
       c.st.h2d_bytes += 12.0 * n;
     }
-    if (l + 1 == D) upload_weights(c, chunk, n);  // the fused leaf pass reads them
+    if (l + 1 == D) {
+      upload_weights(c, chunk, n);  // the fused leaf pass reads them
+      c.cur_parent = d_parent;      // the projected-leaf gather reads them
+      c.cur_digit = reinterpret_cast<const unsigned long long*>(d_digit);
+      if (c.proj_side >= 0 && !c.host_only) {  // sibling blocks of the projected-leaf gather
+        const int GL = c.group_log, W = 1 << GL;
+        const Level& LD = c.prog.levels[D];
+        const int nk = LD.k_hi - LD.k_lo;
+        uint64_t run_mask = 0;
+        for (int k = std::max(0, nk - GL); k < nk; ++k) run_mask |= 15ull << (4 * k);
+        const int64_t ng = (n + W - 1) / W;
+        const size_t goff = c.ring.alloc(ng * 4);
+        int32_t* gp = reinterpret_cast<int32_t*>(c.ring.h(goff));
+        for (int64_t g = 0; g < ng; ++g) {
+          const int64_t j0 = g * W;
+          bool uni = c.proj_fast && j0 + W <= n;
+          for (int r = 0; uni && r < W; ++r) {
+            const Node& N = chunk[j0 + r];
+            uint64_t want = 0;
+            for (int b = 0; b < GL; ++b) want |= (uint64_t)((r >> b) & 1) << (4 * (nk - 1 - b));
+            uni = N.parent == chunk[j0].parent && (N.digit & ~run_mask) == (chunk[j0].digit & ~run_mask) &&
+                  (N.digit & run_mask) == want;
+          }
+          gp[g] = uni ? chunk[j0].parent : -1;
+        }
+        c.ring.commit(goff, ng * 4, c.stream);
+        c.cur_gpar = reinterpret_cast<const int32_t*>(c.ring.d(goff));
+        static const bool dbg = std::getenv("GS_PROJ_DEBUG") != nullptr;
+        if (dbg) {
+          int64_t nu = 0;
+          for (int64_t g = 0; g < ng; ++g) nu += gp[g] >= 0;
+          std::fprintf(stderr, "proj gather: chunk of %lld leaves, %lld/%lld sibling blocks (fast=%d)\n",
+                       (long long)n, (long long)nu, (long long)ng, (int)c.proj_fast);
+        }
+        c.st.h2d_bytes += 4.0 * ng;
+      }
+    }
     // full fan-out chunk: node j is child j % F of parent chunk[0].parent + j / F
     c.uni_p0 = -1;
     if (c.uniform_chunks) {
@@ -1877,6 +2081,12 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "jit_spill_ok") {
       c.jit_spill_ok = (int)std::max<int64_t>(0, value);
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "proj_perm") {
+      c.proj_perm = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "proj_leaf") {
+      c.proj_leaf = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "tail_gather") {
       c.tail_gather = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -2026,7 +2236,8 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
       js += "]}";
     }
     js += "], \"tail\": [" + std::to_string(c.tail_ops[0].size()) + ", " + std::to_string(c.tail_ops[1].size()) +
-          "], \"jit\": \"";
+          "], \"proj_side\": " + std::to_string(c.proj_side) + ", \"proj_swaps\": " +
+          std::to_string(c.proj_swaps.size()) + ", \"jit\": \"";
     for (char ch : c.jit_status) js += (ch == '"' || ch == '\\' || ch == '\n') ? ' ' : ch;
     js += "\"}";
     if (needed) *needed = (int64_t)js.size() + 1;

@@ -588,6 +588,214 @@ gather_grouped4_kernel(const void* A, const void* B, long long a_elems, long lon
 
 
 // ---------------------------------------------------------------------------
+// Projected leaf side (the paper's sibling structure).  At
+// a CZ cut the A-side cross terms are the projectors P0/P1 on the cross
+// qubits C; when the leaf level's other A ops are one-qubit gates on C only,
+// leaf d's A state is (U_C P_d) psi_parent = product over cross qubits q of
+// U_q[x_q, v_q(d)] times psi_parent at x with C's bits set to v(d).  The leaf
+// A pass is then not run at all: the gather reads the parent state directly.
+
+struct ProjProgD {
+  int n;                 // cross gates of the leaf level (<= 8)
+  int side;              // projected side (0 = A, 1 = B)
+  int s[8];              // state bit of cross gate k's qubit on that side
+  int v[8][16];          // digit -> surviving bit of the projector
+  double a[8][16][2];    // digit -> projector value (complex)
+  double u[8][8];        // U_q (2x2 complex, row-major): the qubit's leaf gates in order
+  int n_swap;            // parent states stored permuted: swap address bits (sa_i, sb_i) in order
+  int sa[4], sb[4];
+  int abit[8];           // address bit of cross gate k's qubit in the (permuted) parent layout
+};
+__constant__ ProjProgD g_proj;
+
+// Per-leaf factor and source index of the projected side: leaf digits dg,
+// block-local index x -> coefficient prod_k a_k(d_k) U_k[x_k, v_k(d_k)] and the
+// parent index y = x with every cross qubit set to v_k(d_k).  Tables from
+// shared memory (the lanes of a warp index them by different digits).
+struct ProjSmem {
+  int n, s[8], v[8][16];
+  double a[8][16][2];
+  double u[8][8];
+  int n_swap, sa[4], sb[4], abit[8];
+};
+
+// state index -> address of a permuted parent state (bit swaps, in order)
+__device__ __forceinline__ long long proj_addr(const ProjSmem& t, long long y) {
+  for (int k = 0; k < t.n_swap; ++k) {
+    const long long ba = (y >> t.sa[k]) & 1, bb = (y >> t.sb[k]) & 1;
+    if (ba != bb) y ^= (1LL << t.sa[k]) | (1LL << t.sb[k]);
+  }
+  return y;
+}
+
+__device__ __forceinline__ void proj_coef(const ProjSmem& t, long long x, unsigned long long dg, double& cr,
+                                          double& ci, long long& y) {
+  cr = 1.0, ci = 0.0;
+  y = x;
+  for (int k = 0; k < t.n; ++k) {
+    const int d = (int)((dg >> (4 * k)) & 15ull);
+    const int sb = t.s[k];
+    const int vb = t.v[k][d];
+    const int xb = (int)((x >> sb) & 1);
+    const double* u = t.u[k] + 2 * (2 * xb + vb);
+    const double fr = t.a[k][d][0] * u[0] - t.a[k][d][1] * u[1];
+    const double fi = t.a[k][d][0] * u[1] + t.a[k][d][1] * u[0];
+    const double tr = cr * fr - ci * fi;
+    ci = cr * fi + ci * fr;
+    cr = tr;
+    y = (y & ~(1LL << sb)) | ((long long)vb << sb);
+  }
+}
+
+// Grouped gather with one projected side: the other side's leaves are grouped
+// path-minor (2^GL per run, 4 lanes per request as gather_grouped4_kernel);
+// the projected side's value of leaf j is coef_j * parent_j[y_j].
+// gpar[g] >= 0 marks a "sibling block": the group's 2^GL leaves are the
+// children of parent gpar[g] that share their other digits and take the last
+// GL (radix-2, v(d) = d) cross digits in order, so leaf j of the group needs
+// the parent amplitude at run position j and coef = F(fixed digits) * R(j),
+// both products of per-request 2x2 factors computed once; else every leaf
+// evaluates proj_coef and reads its own amplitude.
+template <typename R, int GL>
+__global__ void __launch_bounds__(256)
+gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_elems, int n_leaves,
+                   int groups_per_y, const double* weights, const int32_t* parent,
+                   const unsigned long long* digits, const int32_t* gpar, const int32_t* ia, const int32_t* ib,
+                   long long n_req, double2* partial) {
+  using V = typename Cx<R>::T;
+  constexpr int W = 1 << GL;
+  constexpr int Q = W / 4;
+  __shared__ ProjSmem tab;
+  if (threadIdx.x == 0) {
+    tab.n = g_proj.n;
+    for (int k = 0; k < 8; ++k) {
+      tab.s[k] = g_proj.s[k];
+      for (int d = 0; d < 16; ++d) {
+        tab.v[k][d] = g_proj.v[k][d];
+        tab.a[k][d][0] = g_proj.a[k][d][0];
+        tab.a[k][d][1] = g_proj.a[k][d][1];
+      }
+      for (int e = 0; e < 8; ++e) tab.u[k][e] = g_proj.u[k][e];
+    }
+    tab.n_swap = g_proj.n_swap;
+    for (int k = 0; k < 4; ++k) tab.sa[k] = g_proj.sa[k], tab.sb[k] = g_proj.sb[k];
+    for (int k = 0; k < 8; ++k) tab.abit[k] = g_proj.abit[k];
+  }
+  __syncthreads();
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = t >> 2;
+  const int sub = (int)(t & 3);
+  if (i >= n_req) return;
+  const int n_groups = (n_leaves + W - 1) >> GL;
+  const int g0 = blockIdx.y * groups_per_y;
+  const int g1 = min(n_groups, g0 + groups_per_y);
+  const bool pa = g_proj.side == 0;
+  const long long xp = pa ? ia[i] : ib[i];  // index on the projected side
+  const long long xg = pa ? ib[i] : ia[i];  // index on the grouped side
+  const V* pg = reinterpret_cast<const V*>(G) + (xg << GL) + sub * Q;
+  const V* ps = reinterpret_cast<const V*>(P);
+  const int nk = tab.n;
+  // factor of cross gate k with digit d at this request: a_k(d) U_k[x_k, v_k(d)]
+  auto factor = [&](int k, int d, double& ar, double& ai) {
+    const int vb = tab.v[k][d], xb = (int)((xp >> tab.s[k]) & 1);
+    const double* u = tab.u[k] + 2 * (2 * xb + vb);
+    ar = tab.a[k][d][0] * u[0] - tab.a[k][d][1] * u[1];
+    ai = tab.a[k][d][0] * u[1] + tab.a[k][d][1] * u[0];
+  };
+  // this lane's run positions r = sub * Q + s2 (digit of gate nk-1-b = bit b of r):
+  // coefficient R(r) and the parent-index bits of the run gates
+  double rr[Q], ri[Q];
+  long long yrun[Q];
+  long long xclr = xp;
+  for (int k = 0; k < nk; ++k) xclr &= ~(1LL << tab.s[k]);
+#pragma unroll
+  for (int s2 = 0; s2 < Q; ++s2) {
+    const int r = sub * Q + s2;
+    double cr = 1.0, ci = 0.0;
+    long long y = 0;
+    for (int b = 0; b < GL && b < nk; ++b) {
+      const int k = nk - 1 - b, bit = (r >> b) & 1;
+      double ar, ai;
+      factor(k, bit, ar, ai);
+      const double tr = cr * ar - ci * ai;
+      ci = cr * ai + ci * ar;
+      cr = tr;
+      y |= (long long)bit << tab.s[k];
+    }
+    rr[s2] = cr, ri[s2] = ci, yrun[s2] = proj_addr(tab, y);  // address bits of the run part
+  }
+  const long long abase = proj_addr(tab, xclr);  // address of x with every cross bit cleared
+  // fixed (non-run) gates, radix 2: per-request factors for d = 0, 1 (<= 2 such gates)
+  double f0r[2][2], f0i[2][2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int d = 0; d < 2; ++d) {
+      f0r[k][d] = 1.0, f0i[k][d] = 0.0;
+      if (k < nk - GL) factor(k, d, f0r[k][d], f0i[k][d]);
+    }
+  double re = 0.0, im = 0.0;
+  for (int g = g0; g < g1; ++g) {
+    const int j0 = g << GL;
+    const Group<V, Q> yv = load_group<V, Q>(pg + (((long long)g * g_elems) << GL));
+    const int pj = gpar[g];
+    if (pj >= 0) {
+      // fixed digits: those of the group's first leaf, gates 0 .. nk - GL - 1
+      const unsigned long long dg = digits[j0];
+      double Fr = 1.0, Fi = 0.0;
+      long long afix = abase;
+      for (int k = 0; k < nk - GL; ++k) {
+        const int d = (int)((dg >> (4 * k)) & 15ull);
+        double ar, ai;
+        if (k == 0 && d < 2) ar = d ? f0r[0][1] : f0r[0][0], ai = d ? f0i[0][1] : f0i[0][0];
+        else if (k == 1 && d < 2) ar = d ? f0r[1][1] : f0r[1][0], ai = d ? f0i[1][1] : f0i[1][0];
+        else factor(k, d, ar, ai);
+        const double tr = Fr * ar - Fi * ai;
+        Fi = Fr * ai + Fi * ar;
+        Fr = tr;
+        afix |= (long long)tab.v[k][d] << tab.abit[k];
+      }
+      const V* pp = ps + (long long)pj * p_elems + afix;
+      V pv[Q];
+#pragma unroll
+      for (int s2 = 0; s2 < Q; ++s2) pv[s2] = pp[yrun[s2]];
+#pragma unroll
+      for (int s2 = 0; s2 < Q; ++s2) {
+        const int j = j0 + sub * Q + s2;
+        const double cr = Fr * rr[s2] - Fi * ri[s2], ci = Fr * ri[s2] + Fi * rr[s2];
+        const double ar = cr * pv[s2].x - ci * pv[s2].y, ai = cr * pv[s2].y + ci * pv[s2].x;
+        const double yr = yv.v[s2].x, yi = yv.v[s2].y;
+        const double w = weights[j];
+        re += w * (ar * yr - ai * yi);
+        im += w * (ar * yi + ai * yr);
+      }
+    } else {
+#pragma unroll
+      for (int s2 = 0; s2 < Q; ++s2) {
+        const int j = j0 + sub * Q + s2;
+        if (j >= n_leaves) continue;
+        double cr, ci;
+        long long y;
+        proj_coef(tab, xp, digits[j], cr, ci, y);
+        const V pv = ps[(long long)parent[j] * p_elems + proj_addr(tab, y)];
+        const double ar = cr * pv.x - ci * pv.y, ai = cr * pv.y + ci * pv.x;
+        const double yr = yv.v[s2].x, yi = yv.v[s2].y;
+        const double w = weights[j];
+        re += w * (ar * yr - ai * yi);
+        im += w * (ar * yi + ai * yr);
+      }
+    }
+  }
+  // the 4 lanes of a request are consecutive, live together and finish together
+  const unsigned m = __activemask();
+  re += __shfl_xor_sync(m, re, 1);
+  im += __shfl_xor_sync(m, im, 1);
+  re += __shfl_xor_sync(m, re, 2);
+  im += __shfl_xor_sync(m, im, 2);
+  if (sub == 0) partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
+}
+
+// ---------------------------------------------------------------------------
 // Request split on the device (split_requests, pathsum.py:122-140): global
 // index -> block-local indices, one shift+mask per run of consecutive qubits.
 

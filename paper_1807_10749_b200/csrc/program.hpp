@@ -64,6 +64,7 @@ struct PassPlan {
   bool fused_gather = false;    // leaf level, last B pass: gather instead of a B store (JIT)
   bool pipelined = false;       // JIT: persistent kernel prefetching the next tile (option pipeline)
   int level = -1;               // path-tree level of the pass
+  std::vector<int> store_perm;  // non-empty: state bit b is stored at address bit store_perm[b] (JIT only)
 };
 
 struct Level {

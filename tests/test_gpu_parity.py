@@ -421,3 +421,48 @@ def test_four_register_bit_passes(ps, name):
         eng.set_option("reg_bits", 5)
         eng.set_option("jit_min_blocks", 3)
     assert rel_l2(got, g["amps_c64"]) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg4v2", "cfg3v2"])
+def test_projected_leaf_side(ps, name):
+    """proj_leaf=1: the projector-only leaf side (CZ cut, A side) is read from its
+    parent state in the gather (no leaf pass); equal to running the leaf pass."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    eng = _engine("c64")
+    got = {}
+    for pj in (0, 1):
+        eng.set_option("proj_leaf", pj)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            assert eng.describe()["proj_side"] == (0 if pj else -1)
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[pj] = (eng.run(plan.x_p, pre[:9], 0, plan.branch_space).amps,
+                       eng.run(plan.x_p, pre[:5], 1, plan.branch_space - 1).amps)
+        finally:
+            eng.set_option("proj_leaf", 1)
+    for a, b in zip(got[0], got[1]):
+        assert rel_l2(b, a) <= 1e-6 and np.abs(a).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg3v2"])
+def test_projected_leaf_permuted_parents(ps, name):
+    """proj_perm=1 (parents of the projected side stored with the sibling-run
+    qubits at the lowest address bits) gives the default sums."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    eng = _engine("c64")
+    got = {}
+    for pm in (0, 1):
+        eng.set_option("proj_perm", pm)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            if pm:
+                assert eng.describe()["proj_swaps"] > 0
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[pm] = eng.run(plan.x_p, pre[:17], 0, plan.branch_space).amps
+        finally:
+            eng.set_option("proj_perm", 0)
+    assert rel_l2(got[1], got[0]) <= 1e-12 and np.abs(got[0]).max() > 0
