@@ -656,14 +656,8 @@ __device__ __forceinline__ void proj_coef(const ProjSmem& t, long long x, unsign
 // the parent amplitude at run position j and coef = F(fixed digits) * R(j),
 // both products of per-request 2x2 factors computed once; else every leaf
 // evaluates proj_coef and reads its own amplitude.
-#ifndef GS_PROJ_U
-#define GS_PROJ_U 4
-#endif
-#ifndef GS_PROJ_MINB
-#define GS_PROJ_MINB 1
-#endif
 template <typename R, int GL>
-__global__ void __launch_bounds__(256, GS_PROJ_MINB)
+__global__ void __launch_bounds__(256)
 gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_elems, int n_leaves,
                    int groups_per_y, const double* weights, const int32_t* parent,
                    const unsigned long long* digits, const int32_t* gpar, const int32_t* ia, const int32_t* ib,
@@ -741,79 +735,54 @@ gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_
       if (k < nk - GL) factor(k, d, f0r[k][d], f0i[k][d]);
     }
   double re = 0.0, im = 0.0;
-  // fixed-digit factor F and parent address of a sibling block with digits dg
-  auto block_fix = [&](unsigned long long dg, double& Fr, double& Fi, long long& afix) {
-    Fr = 1.0, Fi = 0.0;
-    afix = abase;
-    for (int k = 0; k < nk - GL; ++k) {
-      const int d = (int)((dg >> (4 * k)) & 15ull);
-      double ar, ai;
-      if (k == 0 && d < 2) ar = d ? f0r[0][1] : f0r[0][0], ai = d ? f0i[0][1] : f0i[0][0];
-      else if (k == 1 && d < 2) ar = d ? f0r[1][1] : f0r[1][0], ai = d ? f0i[1][1] : f0i[1][0];
-      else factor(k, d, ar, ai);
-      const double tr = Fr * ar - Fi * ai;
-      Fi = Fr * ai + Fi * ar;
-      Fr = tr;
-      afix |= (long long)tab.v[k][d] << tab.abit[k];
-    }
-  };
-  // U groups per round: every load of the round is issued before any is used
-  constexpr int U = GS_PROJ_U;
-  for (int g = g0; g < g1; g += U) {
-    int pj[U];
-    unsigned long long dgs[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int gg = min(g + u, g1 - 1);
-      pj[u] = gpar[gg];
-      dgs[u] = digits[gg << GL];
-    }
-    Group<V, Q> yv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) yv[u] = load_group<V, Q>(pg + (((long long)min(g + u, g1 - 1) * g_elems) << GL));
-    V pv[U][Q];
-    double Fr[U], Fi[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      Fr[u] = 0.0, Fi[u] = 0.0;
-      if (pj[u] >= 0) {
-        long long afix;
-        block_fix(dgs[u], Fr[u], Fi[u], afix);
-        const V* pp = ps + (long long)pj[u] * p_elems + afix;
-#pragma unroll
-        for (int s2 = 0; s2 < Q; ++s2) pv[u][s2] = pp[yrun[s2]];
+  for (int g = g0; g < g1; ++g) {
+    const int j0 = g << GL;
+    const Group<V, Q> yv = load_group<V, Q>(pg + (((long long)g * g_elems) << GL));
+    const int pj = gpar[g];
+    if (pj >= 0) {
+      // fixed digits: those of the group's first leaf, gates 0 .. nk - GL - 1
+      const unsigned long long dg = digits[j0];
+      double Fr = 1.0, Fi = 0.0;
+      long long afix = abase;
+      for (int k = 0; k < nk - GL; ++k) {
+        const int d = (int)((dg >> (4 * k)) & 15ull);
+        double ar, ai;
+        if (k == 0 && d < 2) ar = d ? f0r[0][1] : f0r[0][0], ai = d ? f0i[0][1] : f0i[0][0];
+        else if (k == 1 && d < 2) ar = d ? f0r[1][1] : f0r[1][0], ai = d ? f0i[1][1] : f0i[1][0];
+        else factor(k, d, ar, ai);
+        const double tr = Fr * ar - Fi * ai;
+        Fi = Fr * ai + Fi * ar;
+        Fr = tr;
+        afix |= (long long)tab.v[k][d] << tab.abit[k];
       }
-    }
+      const V* pp = ps + (long long)pj * p_elems + afix;
+      V pv[Q];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (g + u >= g1) break;
-      const int j0 = (g + u) << GL;
-      if (pj[u] >= 0) {
+      for (int s2 = 0; s2 < Q; ++s2) pv[s2] = pp[yrun[s2]];
 #pragma unroll
-        for (int s2 = 0; s2 < Q; ++s2) {
-          const int j = j0 + sub * Q + s2;
-          const double cr = Fr[u] * rr[s2] - Fi[u] * ri[s2], ci = Fr[u] * ri[s2] + Fi[u] * rr[s2];
-          const double ar = cr * pv[u][s2].x - ci * pv[u][s2].y, ai = cr * pv[u][s2].y + ci * pv[u][s2].x;
-          const double yr = yv[u].v[s2].x, yi = yv[u].v[s2].y;
-          const double w = weights[j];
-          re += w * (ar * yr - ai * yi);
-          im += w * (ar * yi + ai * yr);
-        }
-      } else {
+      for (int s2 = 0; s2 < Q; ++s2) {
+        const int j = j0 + sub * Q + s2;
+        const double cr = Fr * rr[s2] - Fi * ri[s2], ci = Fr * ri[s2] + Fi * rr[s2];
+        const double ar = cr * pv[s2].x - ci * pv[s2].y, ai = cr * pv[s2].y + ci * pv[s2].x;
+        const double yr = yv.v[s2].x, yi = yv.v[s2].y;
+        const double w = weights[j];
+        re += w * (ar * yr - ai * yi);
+        im += w * (ar * yi + ai * yr);
+      }
+    } else {
 #pragma unroll
-        for (int s2 = 0; s2 < Q; ++s2) {
-          const int j = j0 + sub * Q + s2;
-          if (j >= n_leaves) continue;
-          double cr, ci;
-          long long y;
-          proj_coef(tab, xp, digits[j], cr, ci, y);
-          const V p1 = ps[(long long)parent[j] * p_elems + proj_addr(tab, y)];
-          const double ar = cr * p1.x - ci * p1.y, ai = cr * p1.y + ci * p1.x;
-          const double yr = yv[u].v[s2].x, yi = yv[u].v[s2].y;
-          const double w = weights[j];
-          re += w * (ar * yr - ai * yi);
-          im += w * (ar * yi + ai * yr);
-        }
+      for (int s2 = 0; s2 < Q; ++s2) {
+        const int j = j0 + sub * Q + s2;
+        if (j >= n_leaves) continue;
+        double cr, ci;
+        long long y;
+        proj_coef(tab, xp, digits[j], cr, ci, y);
+        const V pv = ps[(long long)parent[j] * p_elems + proj_addr(tab, y)];
+        const double ar = cr * pv.x - ci * pv.y, ai = cr * pv.y + ci * pv.x;
+        const double yr = yv.v[s2].x, yi = yv.v[s2].y;
+        const double w = weights[j];
+        re += w * (ar * yr - ai * yi);
+        im += w * (ar * yi + ai * yr);
       }
     }
   }

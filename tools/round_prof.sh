@@ -17,6 +17,6 @@ python tools/launchmap.py gpurun_out/${TAG}_cfg4_describe.json gpurun_out/${TAG}
 TOP=$(awk 'NR==2 {print $1}' gpurun_out/${TAG}_cfg4_launchmap.txt)
 ncu --set full --import-source on --clock-control none -k regex:gsj_.*_p${TOP}\$ --launch-skip 4 --launch-count 1 \
     -o gpurun_out/${TAG}_cfg4_top python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${TAG}_ncu2.log 2>&1
-ncu --set full --clock-control none -k regex:gather_grouped4 --launch-skip 4 --launch-count 1 \
+ncu --set full --clock-control none -k regex:gather_ --launch-skip 4 --launch-count 1 \
     -o gpurun_out/${TAG}_cfg4_gather python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/${TAG}_ncu3.log 2>&1
 ls -la gpurun_out/ | grep $TAG
