@@ -656,8 +656,11 @@ __device__ __forceinline__ void proj_coef(const ProjSmem& t, long long x, unsign
 // the parent amplitude at run position j and coef = F(fixed digits) * R(j),
 // both products of per-request 2x2 factors computed once; else every leaf
 // evaluates proj_coef and reads its own amplitude.
+#ifndef GS_PROJ_MINB
+#define GS_PROJ_MINB 4  // 4 CTAs per SM (<= 64 registers): latency-bound, occupancy pays (71.1k -> 76.8k cfg4)
+#endif
 template <typename R, int GL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, GS_PROJ_MINB)
 gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_elems, int n_leaves,
                    int groups_per_y, const double* weights, const int32_t* parent,
                    const unsigned long long* digits, const int32_t* gpar, const int32_t* ia, const int32_t* ib,
