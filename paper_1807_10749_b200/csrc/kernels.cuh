@@ -612,6 +612,17 @@ __constant__ ProjProgD g_proj;
 // block-local index x -> coefficient prod_k a_k(d_k) U_k[x_k, v_k(d_k)] and the
 // parent index y = x with every cross qubit set to v_k(d_k).  Tables from
 // shared memory (the lanes of a warp index them by different digits).
+// one amplitude read with a 64-byte L2 fetch (scattered reads: no 128-byte over-fetch)
+template <typename V> __device__ __forceinline__ V ldg_l2_64(const V* p) {
+  V v;
+  if constexpr (sizeof(V) == 8) {
+    asm volatile("ld.global.nc.L2::64B.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L2::64B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  }
+  return v;
+}
+
 struct ProjSmem {
   int n, s[8], v[8][16];
   double a[8][16][2];
@@ -761,7 +772,7 @@ gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_
       const V* pp = ps + (long long)pj * p_elems + afix;
       V pv[Q];
 #pragma unroll
-      for (int s2 = 0; s2 < Q; ++s2) pv[s2] = pp[yrun[s2]];
+      for (int s2 = 0; s2 < Q; ++s2) pv[s2] = ldg_l2_64<V>(pp + yrun[s2]);
 #pragma unroll
       for (int s2 = 0; s2 < Q; ++s2) {
         const int j = j0 + sub * Q + s2;
