@@ -749,13 +749,22 @@ gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_
       if (k < nk - GL) factor(k, d, f0r[k][d], f0i[k][d]);
     }
   double re = 0.0, im = 0.0;
+  // the group table entries (parent, digits) of group g + 1 are fetched while
+  // group g is processed: the parent read no longer waits on a table load
+  int pj_next = g0 < g1 ? gpar[g0] : -1;
+  unsigned long long dg_next = g0 < g1 ? digits[g0 << GL] : 0ull;
   for (int g = g0; g < g1; ++g) {
     const int j0 = g << GL;
     const Group<V, Q> yv = load_group<V, Q>(pg + (((long long)g * g_elems) << GL));
-    const int pj = gpar[g];
+    const int pj = pj_next;
+    const unsigned long long dg_cur = dg_next;
+    if (g + 1 < g1) {
+      pj_next = gpar[g + 1];
+      dg_next = digits[(g + 1) << GL];
+    }
     if (pj >= 0) {
       // fixed digits: those of the group's first leaf, gates 0 .. nk - GL - 1
-      const unsigned long long dg = digits[j0];
+      const unsigned long long dg = dg_cur;
       double Fr = 1.0, Fi = 0.0;
       long long afix = abase;
       for (int k = 0; k < nk - GL; ++k) {
