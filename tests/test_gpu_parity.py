@@ -466,3 +466,21 @@ def test_projected_leaf_permuted_parents(ps, name):
         finally:
             eng.set_option("proj_perm", 0)
     assert rel_l2(got[1], got[0]) <= 1e-12 and np.abs(got[0]).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg3v2"])
+def test_projected_leaf_linearity_and_duplicates(ps, name):
+    """With the projected leaf side (cfg4 / cfg3v2 A side): partition linearity,
+    duplicate prefixes counting twice (leaf weights), and agreement with the
+    reference window."""
+    circ, plan, req, _ = configs.build(name, n_req=8192)
+    pre = plan.retained[:40]
+    whole = ps.run_batched(circ, plan, req, prefixes=pre).amps
+    parts = sum(ps.run_batched(circ, plan, req, prefixes=p).amps for p in np.array_split(pre, 3))
+    assert rel_l2(parts, whole) <= 1e-10
+    dup = ps.run_batched(circ, plan, req, prefixes=np.concatenate([pre[:5], pre[:5]])).amps
+    one = ps.run_batched(circ, plan, req, prefixes=pre[:5]).amps
+    assert rel_l2(dup, 2 * one) <= 1e-12
+    g = load_amps(name)
+    got = ps.run_batched(circ, plan, g["requests"], prefixes=g["prefixes"]).amps
+    assert rel_l2(got, g["amps_c64"]) <= C64_TOL
