@@ -256,6 +256,7 @@ struct Ctx {
   std::vector<int> tail_bits[2];
   int proj_leaf = 1;          // option: a projector-only leaf side is read from its parent in the gather
   int proj_perm = 0;          // option: store those parents with the sibling-run bits lowest (no measured gain)
+  int proj_lanes = 4;         // option: lanes per request in the projected-leaf gather (4 or 8)
   int proj_side = -1;         // leaf side evaluated by projection (no leaf passes), -1 none
   const int32_t* cur_parent = nullptr;             // device node tables of the current leaf chunk
   const int32_t* cur_gpar = nullptr;               // per leaf group: shared parent of a sibling block, or -1
@@ -1642,8 +1643,12 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     if (c.proj_side >= 0) {  // one side's leaves come from its parent state
       const int ps = c.proj_side;
       const void* P = (ps == 0 ? c.lvl_a : c.lvl_b)[l - 1].p;
-      auto pk = GL == 4 ? gather_proj_kernel<R, 4> : GL == 3 ? gather_proj_kernel<R, 3> : gather_proj_kernel<R, 2>;
-      const int64_t gxb = (4 * nreq + threads - 1) / threads;
+      // lanes per request: 4 (two leaves per lane) or 8 (one, option proj_lanes)
+      const int lpr = (c.proj_lanes == 8 && GL >= 3) ? 8 : 4;
+      auto pk = lpr == 8 ? (GL == 4 ? gather_proj_kernel<R, 4, 8> : gather_proj_kernel<R, 3, 8>)
+                         : (GL == 4 ? gather_proj_kernel<R, 4, 4>
+                                    : GL == 3 ? gather_proj_kernel<R, 3, 4> : gather_proj_kernel<R, 2, 4>);
+      const int64_t gxb = (lpr * nreq + threads - 1) / threads;
       pk<<<dim3((unsigned)gxb, (unsigned)gy), threads, 0, c.stream>>>(
           P, c.leaf_out[1 - ps].p, 1LL << c.prog.q[ps], 1LL << c.prog.q[1 - ps], (int)n, (int)per_y,
           c.cur_weights, c.cur_parent, c.cur_digit, c.cur_gpar, g_ia, g_ib, nreq,
@@ -2081,6 +2086,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "jit_spill_ok") {
       c.jit_spill_ok = (int)std::max<int64_t>(0, value);
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "proj_lanes") {
+      if (value != 4 && value != 8) throw GsError(GS_ERR_ARG, "proj_lanes must be 4 or 8");
+      c.proj_lanes = (int)value;
     } else if (k == "proj_perm") {
       c.proj_perm = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }

@@ -670,7 +670,7 @@ __device__ __forceinline__ void proj_coef(const ProjSmem& t, long long x, unsign
 #ifndef GS_PROJ_MINB
 #define GS_PROJ_MINB 4  // 4 CTAs per SM (<= 64 registers): latency-bound, occupancy pays (71.1k -> 76.8k cfg4)
 #endif
-template <typename R, int GL>
+template <typename R, int GL, int LPR>
 __global__ void __launch_bounds__(256, GS_PROJ_MINB)
 gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_elems, int n_leaves,
                    int groups_per_y, const double* weights, const int32_t* parent,
@@ -678,7 +678,7 @@ gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_
                    long long n_req, double2* partial) {
   using V = typename Cx<R>::T;
   constexpr int W = 1 << GL;
-  constexpr int Q = W / 4;
+  constexpr int Q = W / LPR;  // leaves per lane
   __shared__ ProjSmem tab;
   if (threadIdx.x == 0) {
     tab.n = g_proj.n;
@@ -697,8 +697,8 @@ gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_
   }
   __syncthreads();
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long i = t >> 2;
-  const int sub = (int)(t & 3);
+  const long long i = t / LPR;
+  const int sub = (int)(t % LPR);
   if (i >= n_req) return;
   const int n_groups = (n_leaves + W - 1) >> GL;
   const int g0 = blockIdx.y * groups_per_y;
@@ -811,10 +811,11 @@ gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_
   }
   // the 4 lanes of a request are consecutive, live together and finish together
   const unsigned m = __activemask();
-  re += __shfl_xor_sync(m, re, 1);
-  im += __shfl_xor_sync(m, im, 1);
-  re += __shfl_xor_sync(m, re, 2);
-  im += __shfl_xor_sync(m, im, 2);
+#pragma unroll
+  for (int o = 1; o < LPR; o <<= 1) {
+    re += __shfl_xor_sync(m, re, o);
+    im += __shfl_xor_sync(m, im, o);
+  }
   if (sub == 0) partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
 }
 
