@@ -232,7 +232,7 @@ struct Ctx {
   int group_log = 3;  // leaves per group = 2^group_log (64-byte request reads in c64)
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
-  int reg_bits = 5;  // register bits per stage for c64 (4 or 5; 0 = per pass by op count)
+  int reg_bits = 6;  // register bits per stage for c64: 4, 5, 0 = per pass by op count, 6 = 4 for halves >= 2^26 amplitudes
   int m4_ops = 30;   // reg_bits = 0: passes with at least this many ops use 4 register bits
   int use_jit = 1;   // specialise passes at load time (NVRTC); interpreter otherwise
   int vec_hbm = 1;   // option: vector (16-byte) HBM stage layouts for specialised passes
@@ -816,6 +816,9 @@ static void schedule_program(Ctx& c) {
         // the op-heavy, non-grouped passes when reg_bits = 0 (auto, m4_ops threshold)
         bool m4 = c.reg_bits == 4;
         if (c.reg_bits == 0) m4 = c.use_jit && !pp.grouped_store && (int)pp.ops.size() >= c.m4_ops;
+        // reg_bits = 6 (auto by state size): 4 register bits (512-thread CTAs, 2 per SM)
+        // for half-states of >= 2^26 amplitudes, whose passes stream from HBM with no L2 reuse
+        if (c.reg_bits == 6) m4 = c.use_jit && !pp.grouped_store && p.q[side] >= 26;
         pp.M = (c.precision == GS_C64 && pp.k >= 5 && !m4) ? 5 : (pp.k >= 4 ? 4 : 0);
         if (pp.M == 0) continue;
         // tile = k state bits + slot bits batching small states, up to 2^13 (c64) /
@@ -2154,7 +2157,8 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       c.m4_ops = (int)std::max<int64_t>(1, value);
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "reg_bits") {
-      if (value != 0 && value != 4 && value != 5) throw GsError(GS_ERR_ARG, "reg_bits must be 0, 4 or 5");
+      if (value != 0 && value != 4 && value != 5 && value != 6)
+        throw GsError(GS_ERR_ARG, "reg_bits must be 0, 4, 5 or 6");
       c.reg_bits = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pass_kernel") {

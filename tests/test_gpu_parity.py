@@ -418,7 +418,7 @@ def test_four_register_bit_passes(ps, name):
     try:
         got = ps.run_batched(circ, plan, g["requests"], prefixes=g["prefixes"]).amps
     finally:
-        eng.set_option("reg_bits", 5)
+        eng.set_option("reg_bits", 6)
         eng.set_option("jit_min_blocks", 3)
     assert rel_l2(got, g["amps_c64"]) <= C64_TOL
 
