@@ -484,3 +484,25 @@ def test_projected_leaf_linearity_and_duplicates(ps, name):
     g = load_amps(name)
     got = ps.run_batched(circ, plan, g["requests"], prefixes=g["prefixes"]).amps
     assert rel_l2(got, g["amps_c64"]) <= C64_TOL
+
+
+def test_projected_leaf_side_complex128(ps):
+    """The projected leaf side in complex128 mode (interpreted passes, fp64 parents):
+    equal to running the leaf pass to fp64 rounding, and to complex64 within 1e-5."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build("cfg4", n_req=4096)
+    eng = _engine("c128")
+    got = {}
+    for pj in (0, 1):
+        eng.set_option("proj_leaf", pj)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            assert eng.describe()["proj_side"] == (0 if pj else -1)
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[pj] = eng.run(plan.x_p, pre[:6], 0, plan.branch_space).amps
+        finally:
+            eng.set_option("proj_leaf", 1)
+    assert rel_l2(got[1], got[0]) <= 1e-12 and np.abs(got[0]).max() > 0
+    c64 = ps.run_batched(circ, plan, req, prefixes=pre[:6]).amps
+    assert rel_l2(c64, got[1]) <= C64_TOL
