@@ -257,6 +257,7 @@ struct Ctx {
   int proj_leaf = 1;          // option: a projector-only leaf side is read from its parent in the gather
   int proj_perm = 0;          // option: store those parents with the sibling-run bits lowest (no measured gain)
   int proj_lanes = 4;         // option: lanes per request in the projected-leaf gather (4 or 8)
+  int slot_store16 = 0;       // option: grouped leaf stores as 16-byte sibling pairs (JIT; measured 0-3% slower)
   int proj_side = -1;         // leaf side evaluated by projection (no leaf passes), -1 none
   const int32_t* cur_parent = nullptr;             // device node tables of the current leaf chunk
   const int32_t* cur_gpar = nullptr;               // per leaf group: shared parent of a sibling block, or -1
@@ -827,7 +828,8 @@ static void schedule_program(Ctx& c) {
         if (pp.grouped_store) pp.K = pp.k + c.group_log;  // the grouped store interleaves 2^G slots
         // complex64 specialised passes use 16-byte HBM accesses (jitgen.inc)
         const bool vec = c.precision == GS_C64 && c.use_jit && c.vec_hbm && (pp.M == 5 || pp.M == 4);
-        pp.stages = schedule_stages(pp, pp.M, vec, pp.grouped_store ? c.group_log : 0);
+        pp.stages = schedule_stages(pp, pp.M, vec, pp.grouped_store ? c.group_log : 0,
+                                    pp.grouped_store && c.slot_store16 && !c.pipeline);
         pp.dev_stage_offset = (int64_t)c.host_pstages.size();
         pp.goff_offset = (int64_t)c.host_gofftab.size();
         for (int t = 0; t < (1 << pp.k); ++t) {
@@ -839,7 +841,7 @@ static void schedule_program(Ctx& c) {
         for (int j = 0; j < (int)pp.lbits.size(); ++j) tpos[pp.lbits[j]] = j;
         for (const StagePlan& sp : pp.stages) {
           PStage ps{};
-          std::vector<int> rpos(pp.k, -1);
+          std::vector<int> rpos(pp.K, -1);  // register position of each tile bit (slot bits included)
           for (int i = 0; i < (int)sp.rb.size(); ++i) ps.rb[i] = (int8_t)sp.rb[i], rpos[sp.rb[i]] = i;
           {  // swizzled shared-tile byte step per register bit (pass_kernel.cuh swz)
             const int lb = c.precision == GS_C64 ? 4 : 3;
@@ -858,7 +860,7 @@ static void schedule_program(Ctx& c) {
             const bool hbm_stage = (si == 0) || (si + 1 == pp.stages.size());
             std::vector<int> tbits;
             for (int j = 0; j < pp.K; ++j)
-              if (j >= pp.k || rpos[j] < 0) tbits.push_back(j);
+              if (rpos[j] < 0) tbits.push_back(j);
             if (pp.grouped_store && si + 1 == pp.stages.size()) {
               // grouped store: slot bits on the lowest lanes -> 2^G leaves x 2^(5-G)
               // amplitudes = 256 contiguous bytes per warp store
@@ -1407,6 +1409,10 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
   if (q > 31) throw GsError(GS_ERR_ARG, "half-states beyond 2^31 amplitudes are not supported");
   if (pp.grouped_store && pp.K - pp.k != c.group_log)
     throw GsError(GS_ERR_ARG, "grouped store needs group_log slot bits");
+  if (!c.host_only && pp.grouped_store && pp.jit_index < 0 && !pp.stages.empty())
+    for (int b : pp.stages.back().rb)
+      if (b >= pp.k)  // the interpreter keeps slot bits on threads
+        throw GsError(GS_ERR_ARG, "16-byte grouped store needs the specialised kernel (set slot_store16=0)");
   for (int j = 0; j < pp.k; ++j) a.lbits[j] = pp.lbits[j];
   for (int j = 0; j < (int)pp.gbits.size(); ++j) a.gbits[j] = pp.gbits[j];
   const int threads = 1 << (a.K - pp.M);
@@ -2088,6 +2094,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       c.uniform_chunks = value ? 1 : 0;
     } else if (k == "jit_spill_ok") {
       c.jit_spill_ok = (int)std::max<int64_t>(0, value);
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "slot_store16") {
+      c.slot_store16 = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "proj_lanes") {
       if (value != 4 && value != 8) throw GsError(GS_ERR_ARG, "proj_lanes must be 4 or 8");

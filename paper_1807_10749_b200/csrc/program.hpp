@@ -174,7 +174,8 @@ inline std::vector<PassPlan> schedule_passes(const std::vector<HostOp>& ops, int
 // and tile bits 3 and 4 may be register bits.  A grouped store (2^G leaves
 // interleaved per amplitude, G >= 3) puts the slot bits on the lowest lanes,
 // so any last stage already writes >= 64-byte runs.
-inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M, bool vec = false, int group_log = 0) {
+inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M, bool vec = false, int group_log = 0,
+                                             bool slot_reg = false) {
   const int k = pp.k;
   std::vector<int> tile_of(64, -1);
   for (int j = 0; j < k; ++j) tile_of[pp.lbits[j]] = j;
@@ -281,6 +282,19 @@ inline std::vector<StagePlan> schedule_stages(const PassPlan& pp, int M, bool ve
     out.push_back(std::move(sp));
     remaining = std::move(deferred);
     first = false;
+  }
+  // grouped store: trade a filler register bit of the last stage for slot bit 0
+  // (tile bit k): sibling leaves s, s + 1 of one amplitude are adjacent in the
+  // grouped layout, so each thread then stores them as one 16-byte float4.
+  // Not when the last stage holds cross ops (their digits are per slot).
+  if (vec && group_log >= 3 && slot_reg && !last_fill.empty()) {
+    bool cross = false;
+    for (const HostOp& op : out.back().ops) cross |= op.cross >= 0;
+    std::vector<int>& rb = out.back().rb;
+    if (!cross && std::find(rb.begin(), rb.end(), k) == rb.end()) {
+      *std::find(rb.begin(), rb.end(), last_fill.back()) = k;
+      std::sort(rb.begin(), rb.end());
+    }
   }
   // 16-byte stores: trade a filler register bit of the last stage for tile bit 0
   if (vec && group_log < 3 && !last_fill.empty()) {

@@ -506,3 +506,25 @@ def test_projected_leaf_side_complex128(ps):
     assert rel_l2(got[1], got[0]) <= 1e-12 and np.abs(got[0]).max() > 0
     c64 = ps.run_batched(circ, plan, req, prefixes=pre[:6]).amps
     assert rel_l2(c64, got[1]) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg2h"])
+def test_grouped_sibling_pair_stores(ps, name):
+    """slot_store16=1 (leaf slot bit 0 in a register: two sibling leaves per
+    16-byte store) writes the same leaves: bitwise equal sums."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    eng = _engine("c64")
+    got = {}
+    for v in (0, 1):
+        eng.set_option("slot_store16", v)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[v] = (eng.run(plan.x_p, pre[:9], 0, plan.branch_space).amps,
+                      eng.run(plan.x_p, pre[:5], 1, plan.branch_space - 1).amps)
+        finally:
+            eng.set_option("slot_store16", 0)
+    for a, b in zip(got[0], got[1]):
+        assert np.array_equal(a, b) and np.abs(a).max() > 0
