@@ -88,6 +88,12 @@ typedef struct gs_stats {
 int gs_abi_version(void);
 int gs_device_count(int* out);
 
+/* Page-locked host memory for result buffers (cudaHostAlloc): a result
+ * downloaded into it is one DMA at full link speed instead of a staged copy
+ * into pageable memory.  gs_host_free releases a pointer from gs_host_alloc. */
+int gs_host_alloc(int64_t bytes, void** out);
+void gs_host_free(void* p);
+
 /* Create a context on `device` (CUDA ordinal) in numeric mode GS_C64/GS_C128. */
 int gs_create(int device, int precision, gs_ctx** out);
 void gs_destroy(gs_ctx* ctx);

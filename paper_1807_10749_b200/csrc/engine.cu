@@ -2002,6 +2002,21 @@ extern "C" {
 
 int gs_abi_version(void) { return GS_ABI_VERSION; }
 
+int gs_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return GS_ERR_ARG;
+  *out = nullptr;
+  if (cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 16), cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return GS_ERR_NOMEM;
+  }
+  return GS_OK;
+}
+
+void gs_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int gs_device_count(int* out) {
   if (!out) return GS_ERR_ARG;
   int n = 0;

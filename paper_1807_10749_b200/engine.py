@@ -40,6 +40,8 @@ EXPORTED_SYMBOLS = (
     "gs_set_requests_global",
     "gs_run_batched",
     "gs_run_full",
+    "gs_host_alloc",
+    "gs_host_free",
 )
 
 
@@ -108,6 +110,9 @@ def _load():
         _F64P, _P, ctypes.c_int32, ctypes.POINTER(GsStats),
     ]
     lib.gs_run_full.argtypes = [_P, _P, _P, ctypes.POINTER(GsStats)]
+    lib.gs_host_alloc.argtypes = [ctypes.c_int64, ctypes.POINTER(_P)]
+    lib.gs_host_free.argtypes = [_P]
+    lib.gs_host_free.restype = None
     if lib.gs_abi_version() != 1:
         raise ImportError("libgridsim_b200.so ABI version mismatch")
     return lib
@@ -124,6 +129,64 @@ def device_count() -> int:
     n = ctypes.c_int(0)
     LIB.gs_device_count(ctypes.byref(n))
     return n.value
+
+
+class _PinnedBlock:
+    """Owner of one page-locked host block; numpy views keep it alive through
+    ``__array_interface__``, and its release returns the block to the pool."""
+
+    def __init__(self, pool, ptr: int, nbytes: int, count: int):
+        self._pool, self.ptr, self.nbytes = pool, ptr, nbytes
+        self.__array_interface__ = {
+            "shape": (count,), "typestr": np.dtype(np.complex128).str, "data": (ptr, False), "version": 3,
+        }
+
+    def __del__(self):
+        pool = self._pool
+        if pool is not None:
+            try:
+                pool._give_back(self.ptr, self.nbytes)
+            except Exception:  # interpreter shutdown
+                pass
+
+
+class _PinnedPool:
+    """Reusable page-locked result buffers (gs_host_alloc): run_batched returns
+    its complex128 amplitudes in them, so the result download is one full-speed
+    DMA; a buffer is reused once every array on it has been released."""
+
+    def __init__(self, keep_bytes: int = 1 << 30):
+        self.free = {}  # nbytes -> [ptr]
+        self.kept = 0
+        self.keep_bytes = keep_bytes
+        self.pid = os.getpid()
+
+    def array(self, count: int) -> np.ndarray | None:
+        if os.getpid() != self.pid:  # pinned memory belongs to the parent's CUDA context
+            self.__init__(self.keep_bytes)
+        nbytes = max(16, 16 * count)
+        lst = self.free.get(nbytes)
+        if lst:
+            ptr = lst.pop()
+            self.kept -= nbytes
+        else:
+            p = _P()
+            if LIB.gs_host_alloc(nbytes, ctypes.byref(p)) != GS_OK or not p.value:
+                return None
+            ptr = p.value
+        return np.asarray(_PinnedBlock(self, ptr, nbytes, count))
+
+    def _give_back(self, ptr: int, nbytes: int):
+        if os.getpid() != self.pid:
+            return
+        if self.kept + nbytes <= self.keep_bytes:
+            self.free.setdefault(nbytes, []).append(ptr)
+            self.kept += nbytes
+        else:
+            LIB.gs_host_free(_P(ptr))
+
+
+_PINNED = _PinnedPool()
 
 
 class EngineError(RuntimeError):
@@ -275,8 +338,12 @@ class Engine:
         bb = np.ascontiguousarray(block_b, dtype=np.int32)
         pre = np.ascontiguousarray(prefixes, dtype=np.int64).ravel()
         ppre = pre if pre.size else np.zeros(1, dtype=np.int64)
-        # every entry is overwritten: no need to zero-fill
-        host = out if out is not None else np.empty(idx.size, dtype=np.complex128)
+        # every entry is overwritten: no need to zero-fill; page-locked when possible
+        host = out
+        if host is None and self.device >= 0 and idx.size:
+            host = _PINNED.array(idx.size)
+        if host is None:
+            host = np.empty(idx.size, dtype=np.complex128)
         if host.dtype != np.complex128 or not host.flags.c_contiguous or host.size != idx.size:
             raise ValueError("output must be a contiguous complex128 array with one entry per request")
         hp = host.view(np.float64) if host.size else None

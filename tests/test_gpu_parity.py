@@ -528,3 +528,26 @@ def test_grouped_sibling_pair_stores(ps, name):
             eng.set_option("slot_store16", 0)
     for a, b in zip(got[0], got[1]):
         assert np.array_equal(a, b) and np.abs(a).max() > 0
+
+
+def test_pinned_result_buffers(ps):
+    """run_batched results live in reused page-locked buffers: a result stays
+    valid (and distinct) while referenced, and released buffers are reused."""
+    import gc
+
+    from paper_1807_10749_b200 import engine
+
+    circ, plan, req, pre = configs.build("cfg3", n_req=4096)
+    a = ps.run_batched(circ, plan, req, prefixes=pre[:4]).amps
+    a_copy = a.copy()
+    b = ps.run_batched(circ, plan, req, prefixes=pre[4:8]).amps
+    assert a.ctypes.data != b.ctypes.data
+    assert np.array_equal(a, a_copy)  # not overwritten by the second call
+    c = ps.run_batched(circ, plan, req, prefixes=pre[:4]).amps
+    assert np.array_equal(c, a_copy)
+    ptr = b.ctypes.data
+    del b
+    gc.collect()
+    d = ps.run_batched(circ, plan, req, prefixes=pre[4:8]).amps
+    assert d.ctypes.data == ptr  # the released block came back
+    assert isinstance(d.base, engine._PinnedBlock)
