@@ -258,6 +258,7 @@ struct Ctx {
   int proj_perm = 0;          // option: store those parents with the sibling-run bits lowest (no measured gain)
   int proj_lanes = 4;         // option: lanes per request in the projected-leaf gather (4 or 8)
   int slot_store16 = 0;       // option: grouped leaf stores as 16-byte sibling pairs (JIT; measured 0-3% slower)
+  int sink_ops = 12;          // option: move a level's trailing pass of <= sink_ops ops into the next level
   int proj_side = -1;         // leaf side evaluated by projection (no leaf passes), -1 none
   const int32_t* cur_parent = nullptr;             // device node tables of the current leaf chunk
   const int32_t* cur_gpar = nullptr;               // per leaf group: shared parent of a sibling block, or -1
@@ -743,6 +744,35 @@ static void schedule_program(Ctx& c) {
   if (c.proj_leaf && c.grouped_leaf && !c.fuse_gather && c.kernel_version == 2)
     for (int side = 0; side < 2 && c.proj_side < 0; ++side)
       if (projectable(c, side)) c.proj_side = side;
+  // working op lists; option sink_ops: a level's trailing pass of at most
+  // sink_ops ops that commute with the next level's cross terms is moved to the
+  // start of that level (after its cross terms), where it can share a pass --
+  // worth it when the next level has few more nodes (sparse prefix levels)
+  std::vector<std::vector<HostOp>> work[2];
+  for (int side = 0; side < 2; ++side) {
+    work[side].resize(p.levels.size());
+    for (size_t l = 0; l < p.levels.size(); ++l) work[side][l] = p.levels[l].ops[side];
+  }
+  if (c.sink_ops > 0)
+    for (int l = 0; l + 2 <= D; ++l)
+      for (int side = 0; side < 2; ++side) {
+        if (p.q[side] == 0) continue;
+        std::vector<PassPlan> ps = schedule_passes(work[side][l], p.q[side], c.kmax(), c.low_bits, true);
+        if (ps.size() < 2 || (int)ps.back().ops.size() > c.sink_ops) continue;
+        const Level& N = p.levels[l + 1];
+        std::vector<HostOp> head, rest;
+        for (const HostOp& op : work[side][l + 1]) (op.cross >= 0 ? head : rest).push_back(op);
+        bool ok = true;
+        for (const HostOp& m : ps.back().ops)
+          for (const HostOp& x : head) ok = ok && !ops_conflict(m, x);
+        if (!ok || N.k_hi <= N.k_lo) continue;
+        std::vector<HostOp> keep;
+        for (size_t i = 0; i + 1 < ps.size(); ++i) keep.insert(keep.end(), ps[i].ops.begin(), ps[i].ops.end());
+        work[side][l] = keep;
+        head.insert(head.end(), ps.back().ops.begin(), ps.back().ops.end());
+        head.insert(head.end(), rest.begin(), rest.end());
+        work[side][l + 1] = head;
+      }
   for (size_t l = 0; l < p.levels.size(); ++l) {
     Level& L = p.levels[l];
     for (int side = 0; side < 2; ++side) {
@@ -755,7 +785,7 @@ static void schedule_program(Ctx& c) {
         L.passes[side].clear();
         continue;
       }
-      L.passes[side] = schedule_passes(L.ops[side], p.q[side], kcap, c.low_bits, true);
+      L.passes[side] = schedule_passes(work[side][l], p.q[side], kcap, c.low_bits, true);
       for (PassPlan& pp : L.passes[side]) pp.level = (int)l;
       if ((int)l == D) extract_tail(c, L, side);
       if ((int)l == D && c.grouped_leaf) {
@@ -2109,6 +2139,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       c.uniform_chunks = value ? 1 : 0;
     } else if (k == "jit_spill_ok") {
       c.jit_spill_ok = (int)std::max<int64_t>(0, value);
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "sink_ops") {
+      c.sink_ops = (int)std::max<int64_t>(0, value);
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "slot_store16") {
       c.slot_store16 = value ? 1 : 0;

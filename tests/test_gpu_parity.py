@@ -551,3 +551,25 @@ def test_pinned_result_buffers(ps):
     d = ps.run_batched(circ, plan, req, prefixes=pre[4:8]).amps
     assert d.ctypes.data == ptr  # the released block came back
     assert isinstance(d.base, engine._PinnedBlock)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg2h", "cfg5"])
+def test_sunk_trailing_passes(ps, name):
+    """sink_ops (a level's small trailing pass moved behind the next level's cross
+    terms, where it commutes) reorders commuting ops only: equal sums."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    window = pre[:2] if name == "cfg5" else pre[:9]
+    branch_hi = 2 if name == "cfg5" else plan.branch_space
+    eng = _engine("c64")
+    got = {}
+    for v in (0, 12):
+        eng.set_option("sink_ops", v)
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[v] = eng.run(plan.x_p, window, 0, branch_hi).amps
+        finally:
+            eng.set_option("sink_ops", 12)
+    assert rel_l2(got[12], got[0]) <= 1e-6 and np.abs(got[0]).max() > 0
