@@ -231,6 +231,17 @@ struct Ctx {
   DevBuf full_state;  // gs_run_full
   int group_log = 3;  // leaves per group = 2^group_log (64-byte request reads in c64)
   DevBuf leaf_out[2];  // grouped path-minor leaf states (see gather_grouped_kernel)
+  // overlap_gather: leaf chunk i's gather runs on gstream while chunk i+1's leaf
+  // passes run on the main stream (double-buffered leaf states, partials, tables)
+  int overlap_gather = 0;     // option
+  bool ovl = false;           // active for the current run
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_leaf = nullptr, ev_g[2] = {nullptr, nullptr};
+  int flip = 0;
+  DevBuf leaf_out2[2], d_partial2, d_tab[2];
+  cudaStream_t gs = nullptr;        // stream of the current gather (null: main stream)
+  DevBuf* part_sel = nullptr;       // partials buffer of the current gather
+  void* leaf_sel[2] = {nullptr, nullptr};
   DevBuf d_packed;  // requests packed as ia | ib << qa (shared-memory gather)
   int reg_bits = 6;  // register bits per stage for c64: 4, 5, 0 = per pass by op count, 6 = 4 for halves >= 2^26 amplitudes
   int m4_ops = 30;   // reg_bits = 0: passes with at least this many ops use 4 register bits
@@ -1535,7 +1546,7 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
     bool first = true;
     for (const PassPlan& pp : L.passes[side]) {
       c.tick("pass launch");
-      void* out = pp.grouped_store ? c.leaf_out[side].p : dsts[side];
+      void* out = pp.grouped_store ? (c.leaf_sel[side] ? c.leaf_sel[side] : c.leaf_out[side].p) : dsts[side];
       if (c.kernel_version == 2 && pp.M > 0)
         launch_pass2<R>(c, side, pp, first ? srcs[side] : dsts[side], out,
                         first ? parent : nullptr, digit, n, root && first);
@@ -1619,6 +1630,7 @@ static void finish_requests(Ctx& c) {
   sort_requests(c, c.side_stream);
   CK(cudaEventRecord(c.req_done, c.side_stream));
   CK(cudaStreamWaitEvent(c.stream, c.req_done, 0));
+  if (c.gstream) CK(cudaStreamWaitEvent(c.gstream, c.req_done, 0));
   c.st.h2d_bytes += 8.0 * n;
   c.st.n_launches += 1;
 }
@@ -1670,7 +1682,13 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     g_ib = reinterpret_cast<const int32_t*>(c.d_ib_s.p);
     used_sorted = true;
   }
+  cudaStream_t gsm = c.stream;  // stream of this gather's kernels
+  DevBuf* pbuf = &c.d_partial;
   if (c.grouped_leaf) {
+    if (c.gs) gsm = c.gs;
+    if (c.part_sel) pbuf = c.part_sel;
+    void* const lf[2] = {c.leaf_sel[0] ? c.leaf_sel[0] : c.leaf_out[0].p,
+                         c.leaf_sel[1] ? c.leaf_sel[1] : c.leaf_out[1].p};
     const int GL = c.group_log;
     const int64_t ng = (n + (1 << GL) - 1) >> GL;
     int64_t gy = std::max<int64_t>(1, (148 * 16) / std::max<int64_t>(1, xblocks));
@@ -1678,7 +1696,7 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     gy = std::min<int64_t>(gy, std::max<int64_t>(1, (256LL << 20) / (16 * std::max<int64_t>(1, nreq))));
     const int64_t per_y = (ng + gy - 1) / gy;
     gy = (ng + per_y - 1) / per_y;
-    c.d_partial.ensure((size_t)gy * nreq * sizeof(double2));
+    pbuf->ensure((size_t)gy * nreq * sizeof(double2));
     if (c.proj_side >= 0) {  // one side's leaves come from its parent state
       const int ps = c.proj_side;
       const void* P = (ps == 0 ? c.lvl_a : c.lvl_b)[l - 1].p;
@@ -1688,10 +1706,10 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
                          : (GL == 4 ? gather_proj_kernel<R, 4, 4>
                                     : GL == 3 ? gather_proj_kernel<R, 3, 4> : gather_proj_kernel<R, 2, 4>);
       const int64_t gxb = (lpr * nreq + threads - 1) / threads;
-      pk<<<dim3((unsigned)gxb, (unsigned)gy), threads, 0, c.stream>>>(
-          P, c.leaf_out[1 - ps].p, 1LL << c.prog.q[ps], 1LL << c.prog.q[1 - ps], (int)n, (int)per_y,
+      pk<<<dim3((unsigned)gxb, (unsigned)gy), threads, 0, gsm>>>(
+          P, lf[1 - ps], 1LL << c.prog.q[ps], 1LL << c.prog.q[1 - ps], (int)n, (int)per_y,
           c.cur_weights, c.cur_parent, c.cur_digit, c.cur_gpar, g_ia, g_ib, nreq,
-          reinterpret_cast<double2*>(c.d_partial.p));
+          reinterpret_cast<double2*>(pbuf->p));
       launch_check("gather_proj_kernel", gxb * gy, threads, 0);
       groups = gy;
     } else {
@@ -1701,9 +1719,9 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
                     : (GL == 4 ? gather_grouped_kernel<R, 4>
                                : GL == 3 ? gather_grouped_kernel<R, 3> : gather_grouped_kernel<R, 2>);
     const int64_t gxb = c.quad_gather ? (4 * nreq + threads - 1) / threads : xblocks;
-    kern<<<dim3((unsigned)gxb, (unsigned)gy), threads, 0, c.stream>>>(
-        c.leaf_out[0].p, c.leaf_out[1].p, 1LL << qa, 1LL << qb, (int)n, (int)per_y,
-        c.cur_weights, g_ia, g_ib, nreq, reinterpret_cast<double2*>(c.d_partial.p));
+    kern<<<dim3((unsigned)gxb, (unsigned)gy), threads, 0, gsm>>>(
+        lf[0], lf[1], 1LL << qa, 1LL << qb, (int)n, (int)per_y,
+        c.cur_weights, g_ia, g_ib, nreq, reinterpret_cast<double2*>(pbuf->p));
     launch_check("gather_grouped_kernel", gxb * gy, threads, 0);
     groups = gy;
     }
@@ -1761,8 +1779,8 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     const double ar = c.kfinal[0][0], ai = c.kfinal[0][1], br = c.kfinal[1][0], bi = c.kfinal[1][1];
     kf = make_double2(ar * br - ai * bi, ar * bi + ai * br);
   }
-  reduce_kernel<<<(unsigned)xblocks, threads, 0, c.stream>>>(
-      reinterpret_cast<const double2*>(c.d_partial.p), (int)groups, nreq, kf,
+  reduce_kernel<<<(unsigned)xblocks, threads, 0, gsm>>>(
+      reinterpret_cast<const double2*>(pbuf->p), (int)groups, nreq, kf,
       reinterpret_cast<double2*>(c.d_acc.p), used_sorted ? reinterpret_cast<const int32_t*>(c.d_perm.p) : nullptr);
   launch_check("reduce_kernel", xblocks, threads, 0);
   c.st.n_gather_launches += 2;
@@ -1851,10 +1869,49 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
               chunk[j].digit == pack_level_digits(c.prog, l + 1, j % F);
       if (uni) c.uni_p0 = chunk[0].parent;
     }
+    int f = -1;  // overlapped gather: buffer set of this leaf chunk
+    if (c.ovl && l + 1 == D) {
+      f = c.flip;
+      c.flip ^= 1;
+      CK(cudaStreamWaitEvent(c.stream, c.ev_g[f], 0));  // set f's previous gather is done
+      // the gather's tables leave the staging ring for set f's own buffer
+      const int64_t ng = (n + (1 << c.group_log) - 1) >> c.group_log;
+      const size_t ow = 0, op = ow + 8 * (size_t)n, od = op + (((4 * (size_t)n) + 15) & ~(size_t)15),
+                   og = od + 8 * (size_t)n, total = og + 4 * (size_t)ng + 16;
+      c.d_tab[f].ensure(total);
+      char* t = static_cast<char*>(c.d_tab[f].p);
+      CK(cudaMemcpyAsync(t + ow, c.cur_weights, 8 * (size_t)n, cudaMemcpyDeviceToDevice, c.stream));
+      CK(cudaMemcpyAsync(t + op, c.cur_parent, 4 * (size_t)n, cudaMemcpyDeviceToDevice, c.stream));
+      CK(cudaMemcpyAsync(t + od, c.cur_digit, 8 * (size_t)n, cudaMemcpyDeviceToDevice, c.stream));
+      c.cur_weights = reinterpret_cast<const double*>(t + ow);
+      c.cur_parent = reinterpret_cast<const int32_t*>(t + op);
+      c.cur_digit = reinterpret_cast<const unsigned long long*>(t + od);
+      if (c.proj_side >= 0 && c.cur_gpar) {
+        CK(cudaMemcpyAsync(t + og, c.cur_gpar, 4 * (size_t)ng, cudaMemcpyDeviceToDevice, c.stream));
+        c.cur_gpar = reinterpret_cast<const int32_t*>(t + og);
+      }
+      for (int side = 0; side < 2; ++side) c.leaf_sel[side] = (f ? c.leaf_out2 : c.leaf_out)[side].p;
+      c.part_sel = f ? &c.d_partial2 : &c.d_partial;
+    }
+    if (c.ovl && l + 1 == D - 1) {  // the projected gathers read this level's parent states
+      CK(cudaStreamWaitEvent(c.stream, c.ev_g[0], 0));
+      CK(cudaStreamWaitEvent(c.stream, c.ev_g[1], 0));
+    }
     run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
                         at(c.lvl_b, l + 1), d_parent, d_digit, false);
     c.uni_p0 = -1;
+    if (f >= 0) {
+      CK(cudaEventRecord(c.ev_leaf, c.stream));
+      CK(cudaStreamWaitEvent(c.gstream, c.ev_leaf, 0));
+      c.gs = c.gstream;
+    }
     descend<R>(c, l + 1, chunk, n);
+    if (f >= 0) {
+      CK(cudaEventRecord(c.ev_g[f], c.gstream));
+      c.gs = nullptr;
+      c.part_sel = nullptr;
+      c.leaf_sel[0] = c.leaf_sel[1] = nullptr;
+    }
   }
 }
 
@@ -1865,7 +1922,7 @@ static void plan_buffers_impl(Ctx& c, int64_t n_leaves);
 static void plan_buffers(Ctx& c, int64_t n_leaves) {
   const std::vector<int64_t> key = {n_leaves, c.n_req, c.mem_budget_mb, (int64_t)c.sched_serial,
                                     c.fused_active ? 1 : 0, c.group_log, c.grouped_leaf ? 1 : 0, c.max_chunk,
-                                    c.host_only ? 1 : 0};
+                                    c.host_only ? 1 : 0, c.overlap_gather};
   if (key == c.plan_key) return;
   plan_buffers_impl(c, n_leaves);
   c.plan_key = key;
@@ -1897,9 +1954,12 @@ static void plan_buffers_impl(Ctx& c, int64_t n_leaves) {
     budget = std::max(budget, 4.0 * pair);
   }
   // largest uniform cap with sum_l min(bound_l, cap) * pair <= budget
+  // grouped leaf states: one (or, overlapping gathers, two) extra leaf chunks
+  const double leaf_sets = c.grouped_leaf ? (c.overlap_gather ? 2.0 : 0.0) : 0.0;
   auto need = [&](double cap) {
     double s = 0;
     for (int l = 0; l <= D; ++l) s += std::min(bound[l], cap) * pair;
+    s += leaf_sets * std::min(bound[D], cap) * pair;
     return s;
   };
   double lo = 1, hi = (double)c.max_chunk;
@@ -1937,6 +1997,8 @@ static void plan_buffers_impl(Ctx& c, int64_t n_leaves) {
     const size_t gsz = (size_t)1 << c.group_log;
     const size_t slots = (size_t)((c.cap[D] + gsz - 1) / gsz) * gsz;
     for (int side = 0; side < 2; ++side) c.leaf_out[side].ensure(slots * ((size_t)1 << p.q[side]) * c.esize());
+    if (c.overlap_gather)
+      for (int side = 0; side < 2; ++side) c.leaf_out2[side].ensure(slots * ((size_t)1 << p.q[side]) * c.esize());
   }
 }
 
@@ -1984,6 +2046,12 @@ static void run_tree(Ctx& c) {
   int64_t n_leaves_bound = (int64_t)c.prefixes.size() * (c.branch_hi - c.branch_lo);
   plan_buffers(c, std::max<int64_t>(1, n_leaves_bound));
   c.st.n_levels = D + 1;
+  c.ovl = c.overlap_gather && c.grouped_leaf && !c.fused_active && !c.profile && !c.host_only && D >= 1;
+  if (c.ovl && !c.gstream) {
+    CK(cudaStreamCreateWithFlags(&c.gstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c.ev_leaf, cudaEventDisableTiming));
+    for (auto& e : c.ev_g) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   if (c.fused_active && !c.host_only && !c.bucket_valid && c.n_req > 0) {
     finish_requests(c);
     build_buckets(c);
@@ -2097,6 +2165,10 @@ void gs_destroy(gs_ctx* ctx) {
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.ev0) cudaEventDestroy(ctx->c.ev0);
+    if (ctx->c.ev_leaf) cudaEventDestroy(ctx->c.ev_leaf);
+    for (auto e : ctx->c.ev_g)
+      if (e) cudaEventDestroy(e);
+    if (ctx->c.gstream) cudaStreamDestroy(ctx->c.gstream);
     if (ctx->c.ev1) cudaEventDestroy(ctx->c.ev1);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.own_stream);
     if (ctx->c.side_stream) {
@@ -2140,6 +2212,8 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "jit_spill_ok") {
       c.jit_spill_ok = (int)std::max<int64_t>(0, value);
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "overlap_gather") {
+      c.overlap_gather = value ? 1 : 0;
     } else if (k == "sink_ops") {
       c.sink_ops = (int)std::max<int64_t>(0, value);
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -2655,6 +2729,10 @@ static void run_body(Ctx& c, int32_t x_p, int64_t n_prefix, const int64_t* prefi
   }
   if (c.precision == GS_C64) gs::run_tree<float>(c);
   else gs::run_tree<double>(c);
+  if (c.ovl) {  // the overlapped gathers finish before the result is read
+    CK(cudaStreamWaitEvent(c.stream, c.ev_g[0], 0));
+    CK(cudaStreamWaitEvent(c.stream, c.ev_g[1], 0));
+  }
   finish_requests(c);  // runs without a gather (no prefixes) still load the requests
   c.st.host_ms_enqueue =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_call).count();

@@ -573,3 +573,28 @@ def test_sunk_trailing_passes(ps, name):
         finally:
             eng.set_option("sink_ops", 12)
     assert rel_l2(got[12], got[0]) <= 1e-6 and np.abs(got[0]).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg3v2"])
+def test_overlapped_gathers_bitwise(ps, name):
+    """overlap_gather=1 (each leaf chunk's gather on a second stream while the
+    next chunk's leaf passes run; double-buffered leaves, partials, tables) gives
+    bitwise the serial sums, including many small chunks and back-to-back runs."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    eng = _engine("c64")
+    got = {}
+    for v in (0, 1):
+        eng.set_option("overlap_gather", v)
+        eng.set_option("max_chunk", 24)  # many leaf chunks per run
+        try:
+            eng.load_program(lowered(circ, plan.cut))
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[v] = [eng.run(plan.x_p, pre[k * 7:(k + 1) * 7], 0, plan.branch_space).amps for k in range(3)]
+            got[v].append(eng.run(plan.x_p, pre[:5], 1, plan.branch_space - 1).amps)
+        finally:
+            eng.set_option("overlap_gather", 0)
+            eng.set_option("max_chunk", 1 << 20)
+    for a, b in zip(got[0], got[1]):
+        assert np.array_equal(a, b) and np.abs(a).max() > 0
