@@ -135,10 +135,10 @@ class _PinnedBlock:
     """Owner of one page-locked host block; numpy views keep it alive through
     ``__array_interface__``, and its release returns the block to the pool."""
 
-    def __init__(self, pool, ptr: int, nbytes: int, count: int):
+    def __init__(self, pool, ptr: int, nbytes: int, count: int, dtype=np.complex128):
         self._pool, self.ptr, self.nbytes = pool, ptr, nbytes
         self.__array_interface__ = {
-            "shape": (count,), "typestr": np.dtype(np.complex128).str, "data": (ptr, False), "version": 3,
+            "shape": (count,), "typestr": np.dtype(dtype).str, "data": (ptr, False), "version": 3,
         }
 
     def __del__(self):
@@ -161,10 +161,10 @@ class _PinnedPool:
         self.keep_bytes = keep_bytes
         self.pid = os.getpid()
 
-    def array(self, count: int) -> np.ndarray | None:
+    def array(self, count: int, dtype=np.complex128) -> np.ndarray | None:
         if os.getpid() != self.pid:  # pinned memory belongs to the parent's CUDA context
             self.__init__(self.keep_bytes)
-        nbytes = max(16, 16 * count)
+        nbytes = max(16, np.dtype(dtype).itemsize * count)
         lst = self.free.get(nbytes)
         if lst:
             ptr = lst.pop()
@@ -174,7 +174,7 @@ class _PinnedPool:
             if LIB.gs_host_alloc(nbytes, ctypes.byref(p)) != GS_OK or not p.value:
                 return None
             ptr = p.value
-        return np.asarray(_PinnedBlock(self, ptr, nbytes, count))
+        return np.asarray(_PinnedBlock(self, ptr, nbytes, count, dtype))
 
     def _give_back(self, ptr: int, nbytes: int):
         if os.getpid() != self.pid:
@@ -365,7 +365,9 @@ class Engine:
             raise RuntimeError("no program loaded")
         dt = np.complex64 if self.precision == 0 else np.complex128
         n = 1 << int(prog.n_a)
-        host = out if out is not None else np.empty(n, dtype=dt)
+        host = out if out is not None else (_PINNED.array(n, dt) if self.device >= 0 else None)
+        if host is None:
+            host = np.empty(n, dtype=dt)
         if host.dtype != dt or not host.flags.c_contiguous or host.size != n:
             raise ValueError(f"output must be a contiguous {np.dtype(dt).name} array of 2^{prog.n_a} entries")
         st = GsStats()
