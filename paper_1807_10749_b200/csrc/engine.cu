@@ -270,6 +270,7 @@ struct Ctx {
   int proj_lanes = 4;         // option: lanes per request in the projected-leaf gather (4 or 8)
   int slot_store16 = 0;       // option: grouped leaf stores as 16-byte sibling pairs (JIT; measured 0-3% slower)
   int sink_ops = 12;          // option: move a level's trailing pass of <= sink_ops ops into the next level
+  int gather_gpy = 0;         // option: leaf groups per gather y-block (0 = auto)
   int proj_side = -1;         // leaf side evaluated by projection (no leaf passes), -1 none
   const int32_t* cur_parent = nullptr;             // device node tables of the current leaf chunk
   const int32_t* cur_gpar = nullptr;               // per leaf group: shared parent of a sibling block, or -1
@@ -1692,8 +1693,14 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     const int GL = c.group_log;
     const int64_t ng = (n + (1 << GL) - 1) >> GL;
     int64_t gy = std::max<int64_t>(1, (148 * 16) / std::max<int64_t>(1, xblocks));
+    // option gather_gpy: groups per y-block (all requests sweep a few groups at a
+    // time, whose parents then stay in L2), bounded by 2 GiB of partials
+    if (c.gather_gpy > 0)
+      gy = std::min<int64_t>((ng + c.gather_gpy - 1) / c.gather_gpy,
+                             std::max<int64_t>(1, (2LL << 30) / (16 * std::max<int64_t>(1, nreq))));
     gy = std::min<int64_t>(gy, ng);
-    gy = std::min<int64_t>(gy, std::max<int64_t>(1, (256LL << 20) / (16 * std::max<int64_t>(1, nreq))));
+    if (c.gather_gpy <= 0)
+      gy = std::min<int64_t>(gy, std::max<int64_t>(1, (256LL << 20) / (16 * std::max<int64_t>(1, nreq))));
     const int64_t per_y = (ng + gy - 1) / gy;
     gy = (ng + per_y - 1) / per_y;
     pbuf->ensure((size_t)gy * nreq * sizeof(double2));
@@ -2212,6 +2219,8 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "jit_spill_ok") {
       c.jit_spill_ok = (int)std::max<int64_t>(0, value);
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "gather_gpy") {
+      c.gather_gpy = (int)std::max<int64_t>(0, value);
     } else if (k == "overlap_gather") {
       c.overlap_gather = value ? 1 : 0;
     } else if (k == "sink_ops") {
