@@ -739,6 +739,9 @@ gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_
     rr[s2] = cr, ri[s2] = ci, yrun[s2] = proj_addr(tab, y);  // address bits of the run part
   }
   const long long abase = proj_addr(tab, xclr);  // address of x with every cross bit cleared
+  // run bit 0 (the last cross gate) at address bit 0: the two run positions of a
+  // lane (r = 2 sub, 2 sub + 1) are adjacent amplitudes, 16-byte aligned
+  const bool pair16 = nk >= 1 && yrun[0] + 1 == yrun[Q - 1] && (yrun[0] & 1) == 0;
   // fixed (non-run) gates, radix 2: per-request factors for d = 0, 1 (<= 2 such gates)
   double f0r[2][2], f0i[2][2];
 #pragma unroll
@@ -780,8 +783,17 @@ gather_proj_kernel(const void* P, const void* G, long long p_elems, long long g_
       }
       const V* pp = ps + (long long)pj * p_elems + afix;
       V pv[Q];
+      if (sizeof(V) == 8 && Q == 2 && pair16) {  // the lane's two run positions are adjacent: one 16-byte load
+        float4 q4;
+        asm volatile("ld.global.nc.L2::64B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(q4.x), "=f"(q4.y), "=f"(q4.z), "=f"(q4.w)
+                     : "l"(reinterpret_cast<const float4*>(pp + yrun[0])));
+        pv[0].x = q4.x, pv[0].y = q4.y;
+        pv[Q - 1].x = q4.z, pv[Q - 1].y = q4.w;
+      } else {
 #pragma unroll
-      for (int s2 = 0; s2 < Q; ++s2) pv[s2] = ldg_l2_64<V>(pp + yrun[s2]);
+        for (int s2 = 0; s2 < Q; ++s2) pv[s2] = ldg_l2_64<V>(pp + yrun[s2]);
+      }
 #pragma unroll
       for (int s2 = 0; s2 < Q; ++s2) {
         const int j = j0 + sub * Q + s2;
