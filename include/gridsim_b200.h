@@ -183,6 +183,41 @@ int gs_run_batched(gs_ctx* ctx, int64_t n_req, const int64_t* idx, int32_t n_qub
  * double pairs in GS_C128 mode) to out_host and/or out_device. */
 int gs_run_full(gs_ctx* ctx, void* out_host, void* out_device, gs_stats* stats);
 
+/* ---- Amplitude consumers --------------------------
+ * Context-free, synchronous, on `device`'s per-thread stream.  Every pointer
+ * may be host or device memory; device inputs are read in place.  The random
+ * streams are numpy's Philox4x64-10 with key [seed, lane] (sampler.py:76-79),
+ * regenerated per draw, so indices and accept decisions are bit-identical to
+ * the reference's; the fp64 sums differ from numpy's only in summation order.
+ * Errors: GS_ERR_ARG (SamplingError / ValueError), message in
+ * gs_sampler_last_error() (per thread). */
+const char* gs_sampler_last_error(void);
+
+/* committed_indices(req, offset) (sampler.py:83-102): `count` draws of the
+ * lane-0 stream starting at draw `offset`, uniform over [0, 2^n_qubits). */
+int gs_committed_indices(int32_t device, int32_t n_qubits, uint64_t seed, int64_t offset, int64_t count,
+                         int64_t* out);
+
+/* sample_basic (mode 0, per_sample = plan_basic(n, eps)) / sample_frugal
+ * (mode 1, per_sample = M') (sampler.py:135-165).  Writes the accepted
+ * indices in batch order to accepted_out (capacity n), their number to
+ * *n_accepted and measured_tail_mass to *tail_mass. */
+int gs_sample(int32_t device, int32_t mode, int32_t n_qubits, int32_t per_sample, uint64_t seed, int64_t n,
+              const int64_t* indices, const double* probs, int64_t* accepted_out, int64_t* n_accepted,
+              double* tail_mass);
+
+/* tail_mass(probs, n_qubits, m_star, resamples, seed) (sampler.py:177-203):
+ * estimate and bootstrap sigma (lane 2 picks, Lemire 32-bit draws). */
+int gs_tail_mass(int32_t device, int32_t n_qubits, int32_t m_star, int32_t resamples, uint64_t seed, int64_t n,
+                 const double* probs, double* estimate, double* sigma);
+
+/* estimate_fidelity(reference, candidate) (pathsum.py:648-664) over two
+ * complex128 batches (re, im pairs) on the same index set. */
+int gs_fidelity(int32_t device, int64_t n, const double* ref_re_im, const double* cand_re_im, double* out);
+
+/* np.abs(amps) ** 2 (cli.py:228): complex128 pairs -> fp64 probabilities. */
+int gs_probabilities(int32_t device, int64_t n, const double* amps_re_im, double* probs_out);
+
 #ifdef __cplusplus
 }
 #endif

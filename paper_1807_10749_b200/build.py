@@ -17,8 +17,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "libgridsim_b200.so")
-SOURCES = ["engine.cu", "pass_kernels.cu", "jit.cu"]
-DEPS = ["engine.cu", "pass_kernels.cu", "jit.cu", "jit.hpp", "jitgen.inc", "kernels.cuh", "program.hpp",
+SOURCES = ["engine.cu", "pass_kernels.cu", "jit.cu", "sampler.cu"]
+DEPS = ["engine.cu", "pass_kernels.cu", "jit.cu", "sampler.cu", "jit.hpp", "jitgen.inc", "kernels.cuh", "program.hpp",
         "pass_kernel.cuh", "pass_kernel.h", "pass_types.h"]
 
 NVCC_FLAGS = [

@@ -26,6 +26,12 @@ GS_C64, GS_C128 = 0, 1
 
 # every symbol include/gridsim_b200.h declares
 EXPORTED_SYMBOLS = (
+    "gs_sampler_last_error",
+    "gs_committed_indices",
+    "gs_sample",
+    "gs_tail_mass",
+    "gs_fidelity",
+    "gs_probabilities",
     "gs_abi_version",
     "gs_device_count",
     "gs_create",
