@@ -9,8 +9,8 @@
 // counter, so every draw is bit-identical to the reference's; only the
 // floating-point sums (tail, bootstrap, fidelity) differ in summation order.
 //
-// All of this is HBM-streaming integer/fp64 work: one thread per entry, grid
-// a multiple of the SM count, no tensor cores.  Pointers may be host or device
+// All of this is HBM-streaming integer/fp64 work: one Philox block (4 or 8
+// draws) per thread, grid-stride loops capped at 16 CTAs per SM, no tensor cores.  Pointers may be host or device
 // memory (cudaPointerGetAttributes decides); device inputs stay in place, so
 // the amplitudes of a gs_run with a device output never leave HBM.
 #include <cuda_runtime.h>
@@ -72,17 +72,6 @@ __device__ __forceinline__ Words4 philox_block(uint64_t block, uint64_t k0, uint
   return o;
 }
 
-__device__ __forceinline__ uint64_t word64(uint64_t i, uint64_t seed, uint64_t lane) {
-  Words4 b = philox_block(i >> 2, seed, lane);
-  return b.w[i & 3];
-}
-
-// next_uint32: the low half of a 64-bit word first, then its high half
-__device__ __forceinline__ uint32_t word32(uint64_t i, uint64_t seed, uint64_t lane) {
-  uint64_t w = word64(i >> 1, seed, lane);
-  return (i & 1) ? uint32_t(w >> 32) : uint32_t(w);
-}
-
 constexpr int kThreads = 256;
 
 int grid_for(int64_t n) {
@@ -94,12 +83,22 @@ int grid_for(int64_t n) {
 }
 
 // ---- kernels ------------------------------------------------------------------
+// One Philox block per thread: 8 draws (32-bit words, n <= 32) or 4 (64-bit).
 __global__ void committed_kernel(int64_t* out, int64_t count, int64_t offset, int n_qubits, uint64_t seed) {
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
-    uint64_t d = uint64_t(offset + i);
-    // Lemire over a power-of-two range never rejects: the top n bits
-    out[i] = n_qubits <= 32 ? int64_t(word32(d, seed, 0) >> (32 - n_qubits))
-                            : int64_t(word64(d, seed, 0) >> (64 - n_qubits));
+  const int per = n_qubits <= 32 ? 8 : 4;
+  const int64_t first = offset / per, last = (offset + count - 1) / per;
+  for (int64_t b = first + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; b <= last;
+       b += int64_t(gridDim.x) * blockDim.x) {
+    Words4 w = philox_block(uint64_t(b), seed, 0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= per) break;
+      const int64_t i = b * per + k - offset;
+      if (i < 0 || i >= count) continue;
+      // Lemire over a power-of-two range never rejects: the top n bits
+      out[i] = per == 8 ? int64_t(uint32_t(k & 1 ? w.w[k >> 1] >> 32 : w.w[k >> 1]) >> (32 - n_qubits))
+                        : int64_t(w.w[k] >> (64 - n_qubits));
+    }
   }
 }
 
@@ -110,24 +109,27 @@ __device__ __forceinline__ double block_sum(double v) {
   return BR(tmp).Sum(v);
 }
 
-// accept flags + per-block tail partials (fixed order: deterministic)
+// accept flags + per-block tail partials (fixed order: deterministic); one
+// Philox block (4 uniforms) per thread
 __global__ void __launch_bounds__(kThreads) sample_kernel(const double* __restrict__ probs, int64_t n, int mode,
                                                           double n_states, double per_sample, uint64_t seed,
                                                           uint8_t* __restrict__ flags, double* __restrict__ partial) {
   double tail = 0.0;
   const double cap = per_sample / n_states;  // m / N (sampler.py:143 / :161)
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    double p = probs[i];
-    double u = double(word64(uint64_t(i), seed, 1) >> 11) * (1.0 / 9007199254740992.0);
-    double ratio = __ddiv_rn(__dmul_rn(p, n_states), per_sample);  // probs * n_states / m
-    bool acc;
-    if (mode == 0) {
-      acc = (p <= cap) && (u < ratio);
-    } else {
-      acc = u < fmin(1.0, ratio);
+  const int64_t n_blocks = (n + 3) / 4;
+  for (int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; b < n_blocks; b += int64_t(gridDim.x) * blockDim.x) {
+    Words4 w = philox_block(uint64_t(b), seed, 1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = 4 * b + k;
+      if (i >= n) break;
+      double p = probs[i];
+      double u = double(w.w[k] >> 11) * (1.0 / 9007199254740992.0);
+      double ratio = __ddiv_rn(__dmul_rn(p, n_states), per_sample);  // probs * n_states / m
+      bool acc = mode == 0 ? (p <= cap) && (u < ratio) : u < fmin(1.0, ratio);
+      flags[i] = acc ? 1 : 0;
+      if (p > cap) tail += p;
     }
-    flags[i] = acc ? 1 : 0;
-    if (p > cap) tail += p;
   }
   double s = block_sum<kThreads>(tail);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
@@ -149,24 +151,35 @@ __global__ void tail_contrib_kernel(const double* __restrict__ probs, int64_t n,
 // Lemire 32-bit bounded draws (numpy buffered_bounded_lemire_uint32): word j
 // is kept when its low product half clears the threshold, else the next word
 // is drawn -- the stream compaction below turns kept words into picks.
-__global__ void bounded_words_kernel(uint64_t start, int64_t count, uint32_t size, uint32_t threshold, uint64_t seed,
+__global__ void bounded_words_kernel(int64_t count, uint32_t size, uint32_t threshold, uint64_t seed,
                                      uint32_t* __restrict__ value, uint8_t* __restrict__ keep) {
-  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < count; j += int64_t(gridDim.x) * blockDim.x) {
-    uint64_t m = uint64_t(word32(start + uint64_t(j), seed, 2)) * size;
-    value[j] = uint32_t(m >> 32);
-    keep[j] = uint32_t(m) >= threshold;
+  const int64_t n_blocks = (count + 7) / 8;  // 8 32-bit words per Philox block
+  for (int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; b < n_blocks; b += int64_t(gridDim.x) * blockDim.x) {
+    Words4 w = philox_block(uint64_t(b), seed, 2);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t j = 8 * b + k;
+      if (j >= count) break;
+      uint32_t u = uint32_t(k & 1 ? w.w[k >> 1] >> 32 : w.w[k >> 1]);
+      uint64_t m = uint64_t(u) * size;
+      value[j] = uint32_t(m >> 32);
+      keep[j] = uint32_t(m) >= threshold;
+    }
   }
 }
 
-// one CTA per bootstrap resample: sum of contrib over its picks
+// bootstrap sums: blockIdx.y = resample, blockIdx.x = chunk of its picks;
+// per-CTA partials are summed on the host in chunk order (deterministic)
 __global__ void __launch_bounds__(kThreads) boot_kernel(const double* __restrict__ contrib,
                                                         const uint32_t* __restrict__ picks, int64_t size,
-                                                        double* __restrict__ boots) {
-  const uint32_t* row = picks + int64_t(blockIdx.x) * size;
+                                                        int64_t chunk, double* __restrict__ partial) {
+  const uint32_t* row = picks + int64_t(blockIdx.y) * size;
+  const int64_t lo = int64_t(blockIdx.x) * chunk;
+  const int64_t hi = lo + chunk < size ? lo + chunk : size;
   double acc = 0.0;
-  for (int64_t i = threadIdx.x; i < size; i += blockDim.x) acc += contrib[row[i]];
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += __ldg(contrib + __ldcs(row + i));
   double s = block_sum<kThreads>(acc);
-  if (threadIdx.x == 0) boots[blockIdx.x] = s;
+  if (threadIdx.x == 0) partial[int64_t(blockIdx.y) * gridDim.x + blockIdx.x] = s;
 }
 
 __global__ void __launch_bounds__(kThreads) fidelity_kernel(const double2* __restrict__ r, const double2* __restrict__ c,
@@ -213,16 +226,19 @@ bool is_device_ptr(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
-// device buffers freed on scope exit
+// Device buffers from the stream-ordered pool (cudaMallocAsync), returned on
+// scope exit: repeated calls reuse pool memory instead of paying
+// cudaMalloc/cudaFree (a device-wide synchronisation) every time.
 struct DevBufs {
+  cudaStream_t stream = cudaStreamPerThread;
   std::vector<void*> ptrs;
   ~DevBufs() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, stream);
   }
   template <class T>
   cudaError_t alloc(T** out, int64_t count) {
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, size_t(count > 0 ? count : 1) * sizeof(T));
+    cudaError_t e = cudaMallocAsync(&p, size_t(count > 0 ? count : 1) * sizeof(T), stream);
     if (e == cudaSuccess) ptrs.push_back(p);
     *out = static_cast<T*>(p);
     return e;
@@ -253,6 +269,15 @@ int copy_out(T* dst, const T* src, int64_t count, cudaStream_t s) {
 int use_device(int32_t device, cudaStream_t* s) {
   SCHECK(cudaSetDevice(device));
   *s = cudaStreamPerThread;
+  // keep up to 4 GiB of freed pool memory for the next call
+  static thread_local int configured = -1;
+  if (configured != device) {
+    cudaMemPool_t pool;
+    SCHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = uint64_t(4) << 30;
+    SCHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    configured = device;
+  }
   return GS_OK;
 }
 
@@ -281,7 +306,7 @@ int gs_committed_indices(int32_t device, int32_t n_qubits, uint64_t seed, int64_
   int64_t* d = out;
   bool dev_out = is_device_ptr(out);
   if (!dev_out) SCHECK(bufs.alloc(&d, count));
-  committed_kernel<<<grid_for(count), kThreads, 0, s>>>(d, count, offset, n_qubits, seed);
+  committed_kernel<<<grid_for(count / 4 + 2), kThreads, 0, s>>>(d, count, offset, n_qubits, seed);
   SCHECK(cudaGetLastError());
   if (!dev_out) {
     rc = copy_out(out, d, count, s);
@@ -312,7 +337,7 @@ int gs_sample(int32_t device, int32_t mode, int32_t n_qubits, int32_t per_sample
   double* partial;
   int64_t* sel;
   int64_t* d_count;
-  const int grid = grid_for(n);
+  const int grid = grid_for((n + 3) / 4);
   SCHECK(bufs.alloc(&flags, n));
   SCHECK(bufs.alloc(&partial, grid));
   SCHECK(bufs.alloc(&sel, n));
@@ -343,7 +368,7 @@ int gs_tail_mass(int32_t device, int32_t n_qubits, int32_t m_star, int32_t resam
   if (n <= 0) return fail(GS_ERR_ARG, "need a non-empty 1-d probability batch");
   if (n > (int64_t(1) << 32)) return fail(GS_ERR_ARG, "bootstrap batches are limited to 2^32 entries");
   if (n_qubits < 1 || n_qubits > 62) return fail(GS_ERR_ARG, "n_qubits must be in [1, 62]");
-  if (resamples < 1) return fail(GS_ERR_ARG, "resamples must be >= 1");
+  if (resamples < 1 || resamples > 65535) return fail(GS_ERR_ARG, "resamples must be in [1, 65535]");
   cudaStream_t s;
   int rc = use_device(device, &s);
   if (rc) return rc;
@@ -383,7 +408,7 @@ int gs_tail_mass(int32_t device, int32_t n_qubits, int32_t m_star, int32_t resam
       SCHECK(round.alloc(&value, words));
       SCHECK(round.alloc(&keep, words));
       SCHECK(round.alloc(&d_count, 1));
-      bounded_words_kernel<<<grid_for(words), kThreads, 0, s>>>(0, words, uint32_t(size), thr, seed, value, keep);
+      bounded_words_kernel<<<grid_for((words + 7) / 8), kThreads, 0, s>>>(words, uint32_t(size), thr, seed, value, keep);
       SCHECK(cudaGetLastError());
       uint32_t* sel;
       SCHECK(round.alloc(&sel, words));
@@ -403,13 +428,24 @@ int gs_tail_mass(int32_t device, int32_t n_qubits, int32_t m_star, int32_t resam
       words = words * 2;
     }
   }
-  double* boots;
-  SCHECK(bufs.alloc(&boots, resamples));
-  boot_kernel<<<resamples, kThreads, 0, s>>>(contrib, picks, n, boots);
+  // enough CTAs to fill the machine: ~8 per SM over all resamples, >= 2048 picks each
+  int64_t chunks = (int64_t(148) * 8 + resamples - 1) / resamples;
+  const int64_t max_chunks = (n + 2047) / 2048;
+  if (chunks > max_chunks) chunks = max_chunks;
+  if (chunks < 1) chunks = 1;
+  if (chunks > 65535) chunks = 65535;
+  const int64_t chunk = (n + chunks - 1) / chunks;
+  chunks = (n + chunk - 1) / chunk;
+  double* bpart;
+  SCHECK(bufs.alloc(&bpart, int64_t(resamples) * chunks));
+  boot_kernel<<<dim3(unsigned(chunks), unsigned(resamples)), kThreads, 0, s>>>(contrib, picks, n, chunk, bpart);
   SCHECK(cudaGetLastError());
-  std::vector<double> hb(resamples);
-  SCHECK(cudaMemcpyAsync(hb.data(), boots, resamples * sizeof(double), cudaMemcpyDeviceToHost, s));
+  std::vector<double> hpart(size_t(resamples) * size_t(chunks));
+  SCHECK(cudaMemcpyAsync(hpart.data(), bpart, hpart.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
   SCHECK(cudaStreamSynchronize(s));
+  std::vector<double> hb(resamples, 0.0);
+  for (int32_t r = 0; r < resamples; ++r)
+    for (int64_t c = 0; c < chunks; ++c) hb[r] += hpart[size_t(r) * size_t(chunks) + size_t(c)];
   if (estimate) *estimate = sum_partials(hp) * scale;
   // boots.std(): population standard deviation (ddof 0)
   double mean = 0.0;

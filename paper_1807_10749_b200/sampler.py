@@ -220,7 +220,9 @@ def probabilities(amps, device: int = 0) -> np.ndarray:
         amps = np.ascontiguousarray(amps, dtype=np.complex128)
         ap, keep, n = amps.ctypes.data, amps, amps.size
     else:
-        ap, keep, n = amps.data_ptr(), amps, amps.numel()
+        # complex128 tensor, or float64 (re, im) pairs
+        ap, keep = amps.data_ptr(), amps
+        n = amps.numel() if amps.is_complex() else amps.numel() // 2
     out = np.empty(n, dtype=np.float64)
     _check(LIB.gs_probabilities(device, n, ap, out.ctypes.data))
     del keep

@@ -185,7 +185,8 @@ def test_device_inputs_stay_on_device():
     idx = B.committed_indices(req)
     amps = (np.random.default_rng(3).standard_normal((idx.size, 2)) / 1024.0).view(np.complex128).ravel()
     p_host = B.probabilities(amps)
-    np.testing.assert_allclose(p_host, np.abs(amps) ** 2, rtol=1e-15, atol=0)
+    # CUDA hypot vs libm hypot: a few ulp apart at most
+    np.testing.assert_allclose(p_host, np.abs(amps) ** 2, rtol=8e-16 * 4, atol=0)
     d_amps = torch.from_numpy(amps.view(np.float64).copy()).cuda()
     np.testing.assert_array_equal(B.probabilities(d_amps), p_host)
     d_p = torch.from_numpy(p_host).cuda()
