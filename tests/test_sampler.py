@@ -211,3 +211,30 @@ def test_device_fidelity():
     assert B.estimate_fidelity_device(ref, ref) == pytest.approx(1.0, rel=1e-14)
     with pytest.raises(ValueError):
         B.estimate_fidelity_device(ref, AmplitudeBatch(idx, np.zeros(idx.size)))
+
+
+def test_abi_argument_errors_without_a_device():
+    """Argument checks happen before any device work, so they run on CPU."""
+    import ctypes
+
+    from paper_1807_10749_b200 import sampler as B
+
+    out = np.empty(4, dtype=np.int64)
+    assert B.LIB.gs_committed_indices(0, 0, 1, 0, 4, out.ctypes.data) == -1
+    assert b"n_qubits" in B.LIB.gs_sampler_last_error()
+    assert B.LIB.gs_committed_indices(0, 10, 1, -1, 4, out.ctypes.data) == -1
+    assert B.LIB.gs_committed_indices(0, 10, 1, 0, 0, out.ctypes.data) == 0  # empty: no work
+    n = ctypes.c_int64(0)
+    t = ctypes.c_double(0)
+    p = np.zeros(7)
+    assert B.LIB.gs_sample(0, 1, 10, 10, 1, 7, out.ctypes.data, p.ctypes.data, out.ctypes.data,
+                           ctypes.byref(n), ctypes.byref(t)) == -1
+    assert b"not a multiple" in B.LIB.gs_sampler_last_error()
+    assert B.LIB.gs_sample(0, 2, 10, 1, 1, 7, out.ctypes.data, p.ctypes.data, out.ctypes.data,
+                           ctypes.byref(n), ctypes.byref(t)) == -1
+    assert B.LIB.gs_tail_mass(0, 10, 10, 0, 1, 7, p.ctypes.data, ctypes.byref(t), ctypes.byref(t)) == -1
+    assert B.LIB.gs_fidelity(0, 0, p.ctypes.data, p.ctypes.data, ctypes.byref(t)) == -1
+    with pytest.raises(B.SamplingError):
+        B.committed_indices(B.SampleRequest(n_qubits=10, count=1), offset=-1)
+    with pytest.raises(B.SamplingError):
+        B.tail_mass(np.zeros((2, 2)), 10)
