@@ -57,7 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [nvcc, *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, src)]
+        # GS_EXTRA_NVCC: extra defines for A/B experiments (e.g. -DGS_PROJ_PREFETCH_G=0)
+        cmd = [nvcc, *NVCC_FLAGS, *os.environ.get("GS_EXTRA_NVCC", "").split(), "-c", "-o", obj,
+               os.path.join(CSRC, src)]
         procs.append((src, obj, subprocess.Popen(cmd, cwd=CSRC, stdout=subprocess.PIPE,
                                                  stderr=subprocess.PIPE, text=True)))
     objs = []
