@@ -1068,7 +1068,8 @@ static void jit_program(Ctx& c) {
     const int m = (int)ids.size();
     const int hw = std::max(1u, std::thread::hardware_concurrency());
     const int n_chunks = std::max(1, std::min(m, std::min(hw, 32)));
-    std::vector<std::string> src(n_chunks, jitgen::prelude());
+    std::vector<std::string> src(n_chunks, std::string(std::getenv("GS_STORE_CS") ? "#define GS_STCS 1\n" : "") +
+                                               jitgen::prelude());
     std::vector<std::vector<int>> members(n_chunks);
     std::vector<std::vector<std::string>> names(n_chunks);
     std::vector<size_t> load(n_chunks, 0);
