@@ -66,3 +66,54 @@ def test_world2_gloo_sum_matches_single_process(tmp_path, name):
     circ, plan, req, pre = configs.build(name)
     want = oracle.run_batched(circ, plan, req, pre)
     np.testing.assert_allclose(got, want, rtol=1e-10, atol=1e-14)
+
+
+def _repro_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1807_10749_b200.distributed import reproducible_sum
+
+    total = reproducible_sum(_order_sensitive_partial, np.arange(1000))
+    if rank == 0:
+        np.save(out_path, total.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _order_sensitive_partial(mine):
+    # magnitudes spread over 16 decades: any change of summation order shows in the bits
+    v = np.zeros(64)
+    for p in mine:
+        rng = np.random.default_rng(int(p))
+        v += rng.standard_normal(64) * 10.0 ** rng.integers(-8, 8, size=64)
+    return torch.from_numpy(v)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_reproducible_sum_is_bitwise_equal_across_world_sizes(tmp_path, world):
+    from paper_1807_10749_b200.distributed import reproducible_sum
+
+    single = reproducible_sum(_order_sensitive_partial, np.arange(1000)).numpy()
+    out = str(tmp_path / "total.npy")
+    mp.spawn(_repro_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    got = np.load(out)
+    assert np.array_equal(got.view(np.uint64), single.view(np.uint64))
+    plain = _order_sensitive_partial(np.arange(1000)).numpy()
+    np.testing.assert_allclose(got, plain, rtol=1e-9, atol=1e-6)
+
+
+
+@pytest.mark.gpu
+def test_reproducible_sharded_run_on_device():
+    """One rank evaluates all 8 fixed slices on the GPU; the slice-order sum is
+    deterministic and matches the plain engine run."""
+    from paper_1807_10749_b200.distributed import run_batched_sharded
+    from paper_1807_10749_b200.pathsum import run_approx
+
+    circ, plan, req, pre = configs.build("cfg1")
+    a = run_batched_sharded(circ, plan, req, device=0, reproducible=True)
+    b = run_batched_sharded(circ, plan, req, device=0, reproducible=True)
+    assert np.array_equal(a.amps.view(np.uint64), b.amps.view(np.uint64))
+    want = run_approx(circ, plan, req, device=0).amps
+    np.testing.assert_allclose(a.amps, want, rtol=1e-9, atol=1e-12)
