@@ -407,6 +407,9 @@ def main():
         "gpu_launches": int(sum(st["n_launches"] for st in stats)),
         "clocks": clk.summary(),
         "nodes_per_step": int(np.mean([st["n_nodes"] for st in stats])),
+        # per-path cost (BASELINE cfg5: "a fixed budget of 2^16 paths with per-path cost reported")
+        "per_path": {"gpu_ms_per_path": 1e3 * world / value if value else None,
+                     "budget_2p16_paths_s": 65536.0 / value if value else None},
     }
     if not args.no_cpu and world == 1:
         procs = args.cpu_procs or min(os.cpu_count() or 1, 32)
