@@ -238,3 +238,25 @@ def test_abi_argument_errors_without_a_device():
         B.committed_indices(B.SampleRequest(n_qubits=10, count=1), offset=-1)
     with pytest.raises(B.SamplingError):
         B.tail_mass(np.zeros((2, 2)), 10)
+
+
+@pytest.mark.gpu
+def test_device_sampling_statistics():
+    """The reference's statistical checks (test_sampler.py:120-140) on the device path."""
+    from paper_1807_10749_b200 import sampler as B
+
+    req = B.SampleRequest(16, count=1000, m_star=10, seed=4)
+    idx = B.committed_indices(req)
+    probs = np.random.default_rng(11).exponential(1.0 / (1 << 16), size=idx.size)
+    assert abs(B.sample_frugal(req, idx, probs).accepted_count - 1000) < 300
+    # one acceptance stream for both modes: every basic accept is a frugal accept when M' < M
+    req_b = B.SampleRequest(12, count=200, mode="basic", epsilon=1e-3, seed=9)
+    m = B.plan_basic(12, 1e-3)
+    idx = B.committed_indices(req_b)
+    probs = np.random.default_rng(1).exponential(1.0 / 4096, size=idx.size)
+    basic = B.sample_basic(req_b, idx, probs)
+    req_f = B.SampleRequest(12, count=200 * m // 10, mode="frugal", m_star=10, seed=9)
+    frugal = B.sample_frugal(req_f, idx[: req_f.batch_size], probs[: req_f.batch_size])
+    assert basic.accepted_count <= frugal.accepted_count
+    assert set(basic.indices.tolist()) <= set(frugal.indices.tolist()) | set(idx[req_f.batch_size:].tolist())
+    assert B.SampleSet(np.array([5]), 4, 1, 0.0).bitstrings == ["0101"]
