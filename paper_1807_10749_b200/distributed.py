@@ -103,19 +103,31 @@ def run_batched_sharded(circuit, plan, requests, prefixes=None, group=None, dst:
 
     if device is None:
         device = torch.cuda.current_device()
-    eng, idx = _engine_for(circuit, plan, requests, device, dtype)
-    pre = plan.retained if prefixes is None else np.asarray(prefixes, dtype=np.int64)
+    from .engine import ENGINES
 
-    def partial(mine):
-        out = torch.zeros(2 * idx.size, dtype=torch.float64, device=f"cuda:{device}")
-        if mine.size:
-            eng.run(plan.x_p, mine, 0, plan.branch_space, out_device_ptr=out.data_ptr(), want_host=False)
-        return out
+    eng = ENGINES.get(device, dtype)
+    with eng.lock:
+        eng, idx = _engine_for(circuit, plan, requests, device, dtype)
+        pre = plan.retained if prefixes is None else np.asarray(prefixes, dtype=np.int64)
+        # run on torch's stream: the partial's allocation, the engine's writes and the
+        # collective that reads them are then ordered by construction
+        eng.set_stream(torch.cuda.current_stream(device).cuda_stream)
+        try:
+            def partial(mine):
+                if not mine.size:
+                    return torch.zeros(2 * idx.size, dtype=torch.float64, device=f"cuda:{device}")
+                out = torch.empty(2 * idx.size, dtype=torch.float64, device=f"cuda:{device}")
+                # accumulate=False: the engine writes every entry of ``out``
+                eng.run(plan.x_p, mine, 0, plan.branch_space, out_device_ptr=out.data_ptr(),
+                        want_host=False)
+                return out
 
-    if reproducible:
-        total = reproducible_sum(partial, pre, group=group)
-    else:
-        total = sharded_sum(partial, pre, group=group, dst=dst)
+            if reproducible:
+                total = reproducible_sum(partial, pre, group=group)
+            else:
+                total = sharded_sum(partial, pre, group=group, dst=dst)
+        finally:
+            eng.set_stream(None)
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     if dst is not None and rank != dst:
         return None

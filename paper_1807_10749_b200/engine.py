@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -226,9 +227,17 @@ class RunResult:
 
 
 class Engine:
-    """One device context: a loaded program, a request set and runs over leaves."""
+    """One device context: a loaded program, a request set and runs over leaves.
+
+    A context holds mutable state (the loaded program, the request set, the
+    run's buffers), so a load -> set requests -> run sequence must not
+    interleave with another thread's.  The library releases the GIL during
+    its calls; callers hold ``engine.lock`` across the whole sequence (the
+    package's entry points do).  The lock is re-entrant.
+    """
 
     def __init__(self, device: int = 0, dtype="c64"):
+        self.lock = threading.RLock()
         self.device = int(device)
         self.precision = precision_code(dtype)
         h = _P()
@@ -415,16 +424,19 @@ class _EngineCache:
     def __init__(self):
         self.pid = None
         self.engines = {}
+        self._lock = threading.Lock()
 
     def get(self, device: int, dtype) -> Engine:
-        if self.pid != os.getpid():
-            self.pid = os.getpid()
-            self.engines = {}
+        """The process's engine for (device, dtype); hold ``engine.lock`` while using it."""
         key = (int(device), precision_code(dtype))
-        eng = self.engines.get(key)
-        if eng is None:
-            eng = self.engines[key] = Engine(device, dtype)
-        return eng
+        with self._lock:
+            if self.pid != os.getpid():
+                self.pid = os.getpid()
+                self.engines = {}
+            eng = self.engines.get(key)
+            if eng is None:
+                eng = self.engines[key] = Engine(device, dtype)
+            return eng
 
 
 ENGINES = _EngineCache()

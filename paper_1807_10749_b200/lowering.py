@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .circuit import Circuit, Cut, GateKind, gate_block, gate_matrix
+from .circuit import Circuit, Cut, gate_block, gate_matrix, kind_name
 from .plan import schmidt_decompose
 
 OP_DIAG1, OP_MAT1, OP_DIAG2, OP_MAT2, OP_CROSS = 0, 1, 2, 3, 4
@@ -87,6 +87,8 @@ def _single(u: np.ndarray, pool: _Pool) -> tuple:
 
 
 def lower_circuit(circuit: Circuit, cut: Cut) -> LoweredProgram:
+    """Lower any circuit record (ours or ``gridsim``'s: gates with ``cycle``,
+    ``kind.value``, ``qubits``, ``matrix``) under any cut record."""
     where_a = {q: j for j, q in enumerate(cut.block_a)}
     where_b = {q: j for j, q in enumerate(cut.block_b)}
     pool = _Pool()
@@ -122,7 +124,7 @@ def lower_circuit(circuit: Circuit, cut: Cut) -> LoweredProgram:
         if len(g.qubits) == 1:
             kind, at = _single(u, pool)
             ops.append((kind, blk, where[g.qubits[0]], -1, g.cycle, at))
-        elif g.kind is GateKind.CZ:
+        elif kind_name(g.kind) == "cz":
             ops.append(
                 (OP_DIAG2, blk, where[g.qubits[0]], where[g.qubits[1]], g.cycle, pool.add(np.diag(u)))
             )

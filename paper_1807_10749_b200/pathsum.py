@@ -36,14 +36,17 @@ ENGINE_NAMES = ("b200", "batched", "perjob")
 
 
 def _engine_for(circuit: Circuit, plan: SimPlan, requests, device: int, dtype):
+    """Engine with ``circuit`` loaded and ``requests`` set; the caller must hold
+    ``eng.lock`` (acquired here, re-entrant) until its runs are done."""
     prog = lowered(circuit, plan.cut)
     if prog.radices != tuple(int(r) for r in plan.radices):
         raise ValueError("plan radices do not match the circuit's cross gates under plan.cut")
     idx = np.asarray(requests, dtype=np.int64).ravel()
     eng = ENGINES.get(device, dtype)
-    eng.load_program(prog)
-    # split_requests (pathsum.py:122-140) runs on the device; IndexError as in the reference
-    eng.set_requests_global(idx, circuit.n_qubits, plan.cut.block_a, plan.cut.block_b)
+    with eng.lock:
+        eng.load_program(prog)
+        # split_requests (pathsum.py:122-140) runs on the device; IndexError as in the reference
+        eng.set_requests_global(idx, circuit.n_qubits, plan.cut.block_a, plan.cut.block_b)
     return eng, idx
 
 
@@ -53,11 +56,12 @@ def _run(circuit, plan, requests, prefixes, branch_lo, branch_hi, device, dtype)
         raise ValueError("plan radices do not match the circuit's cross gates under plan.cut")
     idx = np.asarray(requests, dtype=np.int64).ravel()
     eng = ENGINES.get(device, dtype)
-    eng.load_program(prog)
-    # split_requests (pathsum.py:122-140) runs on the device, overlapped with the
-    # first gate passes; IndexError as in the reference
-    res = eng.run_batched(idx, circuit.n_qubits, plan.cut.block_a, plan.cut.block_b, plan.x_p, prefixes,
-                          branch_lo, branch_hi)
+    with eng.lock:  # one load -> split -> run sequence at a time per context
+        eng.load_program(prog)
+        # split_requests (pathsum.py:122-140) runs on the device, overlapped with the
+        # first gate passes; IndexError as in the reference
+        res = eng.run_batched(idx, circuit.n_qubits, plan.cut.block_a, plan.cut.block_b, plan.x_p,
+                              prefixes, branch_lo, branch_hi)
     return AmplitudeBatch(idx, res.amps)
 
 

@@ -22,7 +22,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .circuit import Circuit, CircuitError, Cut, Gate, GateKind, choose_cut, gate_block, gate_matrix
+from .circuit import (Circuit, CircuitError, Cut, GateKind, as_kind, choose_cut, gate_block,
+                      gate_matrix, kind_name)
 
 _P0 = np.diag([1.0, 0.0]).astype(np.complex128)
 _P1 = np.diag([0.0, 1.0]).astype(np.complex128)
@@ -79,10 +80,10 @@ def schmidt_decompose(gate) -> TermDecomposition:
     exactly; anything else through :func:`_operator_svd_terms`.
     """
     kind, matrix = None, None
-    if isinstance(gate, Gate):
-        kind, matrix = gate.kind, gate_matrix(gate)
-    elif isinstance(gate, GateKind):
-        kind = gate
+    if hasattr(gate, "kind") and hasattr(gate, "qubits"):  # a gate record (ours or gridsim's)
+        kind, matrix = as_kind(gate.kind), gate_matrix(gate)
+    elif hasattr(gate, "value") or isinstance(gate, str):  # a gate kind
+        kind = as_kind(gate)
     else:
         matrix = np.asarray(gate, dtype=np.complex128)
         if matrix.shape != (4, 4):
@@ -94,7 +95,11 @@ def schmidt_decompose(gate) -> TermDecomposition:
             kind, [(_P0, _P0), (_P1, _P1), (1j * _RAISE, _LOWER), (1j * _LOWER, _RAISE)]
         )
     if matrix is None:
-        matrix = gate_matrix(Gate(0, kind, (0, 1)))
+        from .circuit import GATE_TABLE
+
+        matrix = GATE_TABLE[kind_name(kind)][1]
+        if matrix is None or matrix.shape != (4, 4):
+            raise ValueError(f"{kind_name(kind)!r} is not a two-qubit gate with a fixed matrix")
     return TermDecomposition(kind or GateKind.GENERIC_2Q, _operator_svd_terms(matrix))
 
 

@@ -55,9 +55,32 @@ def _check(code: int):
         raise RuntimeError(msg)
 
 
-def _addr(x, dtype):
+_TORCH_DTYPE_NAMES = {np.dtype(np.int64): "torch.int64", np.dtype(np.float64): "torch.float64",
+                      np.dtype(np.complex128): "torch.complex128"}
+
+
+def _device_tensor(x, dtype, device: int | None = None):
+    """Check a CUDA tensor handed to the sampler kernels: element type, layout and
+    device must be what the kernel reads (a float32/int32/complex64 tensor would
+    be read with 8/16-byte strides past its end), and the producer's queued work
+    must be complete -- the sampler runs on its own stream."""
+    want = _TORCH_DTYPE_NAMES[np.dtype(dtype)]
+    if str(x.dtype) != want:
+        raise SamplingError(f"device tensor has dtype {x.dtype}, the sampler needs {want}")
+    if not x.is_contiguous():
+        raise SamplingError("device tensor must be contiguous")
+    if device is not None and x.device.index is not None and x.device.index != device:
+        raise SamplingError(f"tensor is on cuda:{x.device.index}, the request names device {device}")
+    import torch
+
+    torch.cuda.current_stream(x.device).synchronize()
+    return x
+
+
+def _addr(x, dtype, device: int | None = None):
     """(pointer, keep-alive, length) of a numpy array or a CUDA tensor."""
     if hasattr(x, "data_ptr") and getattr(x, "is_cuda", False):
+        x = _device_tensor(x, dtype, device)
         return x.data_ptr(), x, x.numel()
     arr = np.ascontiguousarray(x, dtype=dtype)
     return arr.ctypes.data, arr, arr.size
@@ -158,8 +181,8 @@ def _check_batch(indices, probs, per_sample: int):
 
 def _sample(req: SampleRequest, mode: int, per_sample: int, indices, probs) -> SampleSet:
     indices, probs, n = _check_batch(indices, probs, per_sample)
-    ip, ikeep, _ = _addr(indices, np.int64)
-    pp, pkeep, _ = _addr(probs, np.float64)
+    ip, ikeep, _ = _addr(indices, np.int64, req.device)
+    pp, pkeep, _ = _addr(probs, np.float64, req.device)
     out = np.empty(n, dtype=np.int64)
     count = ctypes.c_int64(0)
     tail = ctypes.c_double(0.0)
@@ -200,7 +223,7 @@ def tail_mass(probs, n_qubits: int, m_star: int = DEFAULT_FRUGAL_M, resamples: i
         probs = np.asarray(probs, dtype=np.float64)
     if len(probs.shape) != 1 or int(probs.shape[0]) == 0:
         raise SamplingError("need a non-empty 1-d probability batch")
-    pp, keep, n = _addr(probs, np.float64)
+    pp, keep, n = _addr(probs, np.float64, device)
     est = ctypes.c_double(0.0)
     sig = ctypes.c_double(0.0)
     _check(LIB.gs_tail_mass(device, n_qubits, m_star, resamples, _seed(seed), n, pp, ctypes.byref(est),
@@ -221,8 +244,15 @@ def probabilities(amps, device: int = 0) -> np.ndarray:
         ap, keep, n = amps.ctypes.data, amps, amps.size
     else:
         # complex128 tensor, or float64 (re, im) pairs
-        ap, keep = amps.data_ptr(), amps
-        n = amps.numel() if amps.is_complex() else amps.numel() // 2
+        if amps.is_complex():
+            keep = _device_tensor(amps, np.complex128, device)
+            n = amps.numel()
+        else:
+            keep = _device_tensor(amps, np.float64, device)
+            if amps.numel() % 2:
+                raise SamplingError("float64 (re, im) pairs need an even element count")
+            n = amps.numel() // 2
+        ap = keep.data_ptr()
     out = np.empty(n, dtype=np.float64)
     _check(LIB.gs_probabilities(device, n, ap, out.ctypes.data))
     del keep

@@ -80,8 +80,9 @@ def run_full(
         raise MemoryBudgetError(f"state of {n} qubits exceeds the 2^31-amplitude block limit")
     del slice_bytes
     eng = ENGINES.get(device, dtype)
-    eng.load_program(lowered(circuit, full_cut(circuit)))
-    return StateBlock(n, eng.run_full().amps)
+    with eng.lock:
+        eng.load_program(lowered(circuit, full_cut(circuit)))
+        return StateBlock(n, eng.run_full().amps)
 
 
 def fetch_amplitudes(state: StateBlock, indices) -> AmplitudeBatch:

@@ -288,37 +288,71 @@ def full_state_cases():
     save("cfg2_full", requests=req, exact=exact, seconds=time.time() - t)
 
 
+def _heavy_plan(name):
+    base = gen(7, 8, 40, "v1")
+    if name == "cfg5f":
+        circ = fsim_variant(base)
+        plan = ps.make_plan(circ, fidelity=256 / 4**31, x_p=31, x_b=4, seed=0)
+        return circ, plan, plan.retained
+    circ = base
+    head = np.load(os.path.join(DATA, "cfg5_retained_head.npy"))
+    from gridsim.pathsum import SimPlan
+    p0 = ps.make_plan(circ, fidelity=1e-30, seed=0)
+    plan = SimPlan(p0.cut, 0.005, p0.radices, p0.x_p, p0.x_b, p0.d_p, p0.d_b, 0, head)
+    return circ, plan, head
+
+
+HEAVY_BRANCHES = {"cfg5": (0, 3), "cfg5f": (0, 3)}
+HEAVY_NREQ = 2048
+
+
+def heavy_one(name, branch):
+    """One reference run_path at 28|28 (about 30-50 CPU-minutes, ~10 GB): the path
+    (first retained prefix, branch) of cfg5 / cfg5f, saved as a part file."""
+    circ, plan, pre = _heavy_plan(name)
+    req = challenge_indices(circ.n_qubits, 10**6, 12345)[:HEAVY_NREQ]
+    pid = int(pre[0]) * plan.branch_space + branch
+    t = time.time()
+    amps = ps.run_path(circ, plan, pid, req).amps
+    os.makedirs(os.path.join(AMPS, "_parts"), exist_ok=True)
+    np.savez(os.path.join(AMPS, "_parts", f"{name}_{branch}.npz"), requests=req, path_id=pid,
+             amps=amps, seconds=time.time() - t, digits=np.array(ps.path_digits(pid, plan.radices)))
+    print(name, branch, "path", pid, "took", round(time.time() - t, 1), "s", flush=True)
+
+
+def heavy_merge(name):
+    parts = [np.load(os.path.join(AMPS, "_parts", f"{name}_{b}.npz")) for b in HEAVY_BRANCHES[name]]
+    save(name, requests=parts[0]["requests"],
+         path_ids=np.array([int(p["path_id"]) for p in parts], dtype=np.int64),
+         path_amps=np.stack([p["amps"] for p in parts]),
+         seconds=np.array([float(p["seconds"]) for p in parts]))
+
+
 def heavy_cases(which=("cfg5", "cfg5f")):
-    """cfg5 windows at 28|28 (hours of CPU; 2 GiB half-states)."""
-    for name, fs in (("cfg5", False), ("cfg5f", True)):
-        if name not in which:
-            continue
-        base = gen(7, 8, 40, "v1")
-        circ = fsim_variant(base) if fs else base
-        if fs:
-            plan = ps.make_plan(circ, fidelity=256 / 4**31, x_p=31, x_b=4, seed=0)
-            pre = plan.retained[:1]
-        else:
-            head = np.load(os.path.join(DATA, "cfg5_retained_head.npy"))
-            from gridsim.pathsum import SimPlan
-            p0 = ps.make_plan(circ, fidelity=1e-30, seed=0)
-            plan = SimPlan(p0.cut, 0.005, p0.radices, p0.x_p, p0.x_b, p0.d_p, p0.d_b, 0, head)
-            pre = head[:1]
-        req = challenge_indices(circ.n_qubits, 10**6, 12345)[:2048]
-        t = time.time()
-        branches = min(plan.branch_space, 4)
-        # leading branches of the first prefix, one path at a time
-        pids = [int(pre[0]) * plan.branch_space + b for b in range(branches)]
-        amps = np.stack([ps.run_path(circ, plan, p, req).amps for p in pids])
-        save(name, requests=req, path_ids=np.array(pids, dtype=np.int64), path_amps=amps,
-             seconds=time.time() - t)
+    """cfg5 / cfg5f per-path reference amplitudes at 28|28 (hours of CPU; 2 GiB
+    half-states). Each path runs in its own process (``--heavy-one name:branch``)
+    so they can run side by side; ``--heavy-merge`` writes amps/<name>.npz."""
+    for name in which:
+        for b in HEAVY_BRANCHES[name]:
+            heavy_one(name, b)
+        heavy_merge(name)
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--heavy", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--heavy-one", default="")
+    ap.add_argument("--heavy-merge", default="")
     args = ap.parse_args()
+    if args.heavy_one:
+        nm, br = args.heavy_one.split(":")
+        heavy_one(nm, int(br))
+        sys.exit(0)
+    if args.heavy_merge:
+        for nm in args.heavy_merge.split(","):
+            heavy_merge(nm)
+        sys.exit(0)
     if args.heavy:
         heavy_cases(tuple(args.only.split(",")) if args.only else ("cfg5", "cfg5f"))
         sys.exit(0)

@@ -117,3 +117,54 @@ def test_reproducible_sharded_run_on_device():
     assert np.array_equal(a.amps.view(np.uint64), b.amps.view(np.uint64))
     want = run_approx(circ, plan, req, device=0).amps
     np.testing.assert_allclose(a.amps, want, rtol=1e-9, atol=1e-12)
+
+
+def _device_worker(rank, world, port, name, window, out_dir):
+    """One rank of the product path: run_batched_sharded on cuda:0 over gloo."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1807_10749_b200.distributed import run_batched_sharded
+
+    circ, plan, req, _ = configs.build(name)
+    pre = plan.retained[:window]
+    plain = run_batched_sharded(circ, plan, req, prefixes=pre, device=0, dst=None)
+    repro = run_batched_sharded(circ, plan, req, prefixes=pre, device=0, reproducible=True)
+    np.save(os.path.join(out_dir, f"plain{rank}.npy"), plain.amps)
+    np.save(os.path.join(out_dir, f"repro{rank}.npy"), repro.amps)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,window", [("cfg3", 64), ("cfg1", None)])
+def test_world2_product_path_on_device(tmp_path, name, window):
+    """run_batched_sharded itself with two ranks (two processes sharing cuda:0;
+    the reduce runs over gloo on the CUDA partials -- the box has one GPU, so
+    NCCL's one-rank-per-GPU rule leaves gloo as the two-rank transport).  Plain
+    mode equals the one-process engine run; the reproducible mode is bitwise
+    equal to its world-1 result (orchestrator.py:340-342 fold semantics)."""
+    from paper_1807_10749_b200.distributed import run_batched_sharded
+    from paper_1807_10749_b200.pathsum import run_batched
+
+    circ, plan, req, _ = configs.build(name)
+    pre = plan.retained if window is None else plan.retained[:window]
+    out = str(tmp_path)
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_device_worker, args=(r, 2, port, name, window or len(pre), out))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    single = run_batched(circ, plan, req, prefixes=pre).amps
+    world1 = run_batched_sharded(circ, plan, req, prefixes=pre, device=0, reproducible=True).amps
+    for r in range(2):
+        plain = np.load(os.path.join(out, f"plain{r}.npy"))
+        repro = np.load(os.path.join(out, f"repro{r}.npy"))
+        assert np.linalg.norm(single) > 0
+        assert np.linalg.norm(plain - single) <= 1e-12 * np.linalg.norm(single)
+        assert np.array_equal(repro.view(np.uint64), world1.view(np.uint64))
