@@ -272,6 +272,13 @@ struct Ctx {
   int sink_ops = 12;          // option: move a level's trailing pass of <= sink_ops ops into the next level
   int gather_gpy = 0;         // option: leaf groups per gather y-block (0 = auto)
   int proj_side = -1;         // leaf side evaluated by projection (no leaf passes), -1 none
+  int proj_fuse = 1;          // option: fuse the other side's last leaf pass with the projected gather (JIT)
+  int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
+  int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
+  bool proj_fused_active = false;  // the fused projected-leaf pass is compiled for the loaded program
+  int64_t pf_rows = 0;        // partial rows written by the current leaf chunk's fused pass
+  DevBuf d_proj;              // device copy of ProjProgD for the fused pass
+  DevBuf d_pftab, d_pfaoff, d_bmeta;  // fused pass: per-group factor tables, per-bucket-slot request data
   const int32_t* cur_parent = nullptr;             // device node tables of the current leaf chunk
   const int32_t* cur_gpar = nullptr;               // per leaf group: shared parent of a sibling block, or -1
   bool proj_fast = false;                          // run gates radix 2 with v(d) = d
@@ -804,6 +811,11 @@ static void schedule_program(Ctx& c) {
         L.passes[side].back().grouped_store = true;
         if (side == 1 && c.fuse_gather && c.group_log == 3 && c.precision == GS_C64)
           L.passes[side].back().fused_gather = true;
+        const int nk = L.k_hi - L.k_lo;
+        PassPlan& lp = L.passes[side].back();
+        if (c.proj_fuse && c.proj_side == 1 - side && c.precision == GS_C64 && c.use_jit && !c.pipeline &&
+            c.group_log == 3 && nk >= 1 && nk <= 5 && c.tail_ops[side].empty())
+          lp.proj_fused = true;
       }
       for (PassPlan& pp : L.passes[side]) {
         pp.dev_op_offset = (int64_t)c.host_devops.size();
@@ -967,7 +979,11 @@ static void schedule_program(Ctx& c) {
   // amplitudes are one contiguous run for the gather
   c.proj_swaps.clear();
   c.proj_perm_pass = nullptr;
-  if (c.proj_perm && c.proj_side >= 0 && D >= 2 && c.precision == GS_C64 && c.use_jit && !c.pipeline) {
+  bool pf_planned = false;
+  if (c.proj_side >= 0 && D >= 1)
+    for (const PassPlan& pp : p.levels[D].passes[1 - c.proj_side]) pf_planned |= pp.proj_fused;
+  if ((c.proj_perm || pf_planned) && c.proj_side >= 0 && D >= 2 && c.precision == GS_C64 && c.use_jit &&
+      !c.pipeline) {
     const int ps = c.proj_side, q = p.q[ps];
     Level& LP = p.levels[D - 1];
     const Level& LD = p.levels[D];
@@ -1025,6 +1041,7 @@ template <typename T> static void upload(Ctx& c, DevBuf& b, const std::vector<T>
 // module.  Failure keeps the interpreter kernels and records why.
 static void jit_program(Ctx& c) {
   c.fused_active = false;
+  c.proj_fused_active = false;
   c.bucket_valid = false;
   for (JitModule* m : c.jit_mods) jit_release(m);
   c.jit_mods.clear();
@@ -1052,7 +1069,7 @@ static void jit_program(Ctx& c) {
   c.jit_smem.assign(n, 0);
   c.jit_loc.assign(n, {0, 0});
   c.jit_occ.assign(n, 1);
-  for (PassPlan* pp : order) pp->pipelined = c.pipeline && !pp->fused_gather;
+  for (PassPlan* pp : order) pp->pipelined = c.pipeline && !pp->fused_gather && !pp->proj_fused;
   // compile passes `ids` with a register bound for `min_blocks` CTAs/SM, in
   // chunks compiled concurrently (~source-size balanced, up to the core count)
   auto compile = [&](const std::vector<int>& ids, int min_blocks, std::string& err) -> bool {
@@ -1060,9 +1077,15 @@ static void jit_program(Ctx& c) {
     for (size_t t = 0; t < ids.size(); ++t) {
       PassPlan& pp = *order[ids[t]];
       size_t smem = 0;
-      kernels[t] = pp.pipelined ? jitgen::pass_kernel_pipe(c, pp, 0, smem)
-                                : jitgen::pass_kernel(c, pp, 0, smem, pp.fused_gather,
-                                                      pp.M == 4 && min_blocks > 2 ? 2 : min_blocks);
+      if (pp.proj_fused) {
+        const Level& LD = c.prog.levels[pp.level];
+        kernels[t] = jitgen::proj_fused_kernel(c, pp, 0, smem, c.pf_u, LD.k_hi - LD.k_lo,
+                                               min_blocks > 0 ? c.pf_min_blocks : 0);
+      } else {
+        kernels[t] = pp.pipelined ? jitgen::pass_kernel_pipe(c, pp, 0, smem)
+                                  : jitgen::pass_kernel(c, pp, 0, smem, pp.fused_gather,
+                                                        pp.M == 4 && min_blocks > 2 ? 2 : min_blocks);
+      }
       c.jit_smem[ids[t]] = smem;
     }
     const int m = (int)ids.size();
@@ -1165,6 +1188,7 @@ static void jit_program(Ctx& c) {
   const int n_chunks = (int)c.jit_mods.size();
   for (int i = 0; i < n; ++i) order[i]->jit_index = i;
   for (PassPlan* pp : order) c.fused_active |= pp->fused_gather;
+  for (PassPlan* pp : order) c.proj_fused_active |= pp->proj_fused;
   c.jit_status = "jit: " + std::to_string(n) + " pass kernels (" + std::to_string(n_spill) +
                  " recompiled without the register bound), " + std::to_string(n_chunks) + " modules compiled in " +
                  std::to_string(c.jit_seconds) + " s";
@@ -1292,6 +1316,8 @@ static void upload_program(Ctx& c) {
       }
     }
     CK(cudaMemcpyToSymbol(g_proj, &pj, sizeof pj));
+    c.d_proj.ensure(sizeof pj);
+    CK(cudaMemcpy(c.d_proj.p, &pj, sizeof pj, cudaMemcpyHostToDevice));
   }
 }
 
@@ -1496,6 +1522,32 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
     const size_t jsm = c.jit_smem[pp.jit_index];
     const auto loc = c.jit_loc[pp.jit_index];
     int64_t grid = blocks;
+    if (pp.proj_fused) {  // fused projected-leaf pass: the group's factor table, then the pass
+      const int ps = c.proj_side;
+      const int D = (int)c.prog.levels.size() - 1;
+      const int nk = c.prog.levels[D].k_hi - c.prog.levels[D].k_lo;
+      const int64_t ng = (n_states + 7) >> 3;
+      c.pf_rows = ng;
+      if (c.n_req <= 0) return;
+      c.d_pftab.ensure((size_t)ng * ((size_t)8 << nk) * sizeof(float2));
+      c.d_pfaoff.ensure((size_t)ng * 8 * sizeof(long long));
+      c.d_partial.ensure(std::max<size_t>((size_t)ng * (size_t)c.n_req * sizeof(double2), 16));
+      const void* P = (ps == 0 ? c.lvl_a : c.lvl_b)[D - 1].p;
+      pf_table_kernel<<<(unsigned)ng, 256, 0, c.stream>>>(reinterpret_cast<const unsigned long long*>(digit),
+                                                        c.cur_parent, c.cur_weights, n_states,
+                                                        1LL << c.prog.q[ps],
+                                                        reinterpret_cast<float2*>(c.d_pftab.p),
+                                                        reinterpret_cast<long long*>(c.d_pfaoff.p));
+      launch_check("pf_table_kernel", ng, 256, 0);
+      c.st.n_launches++;
+      j.bstart = reinterpret_cast<const int32_t*>(c.d_bstart.p);
+      j.partial = c.d_partial.p;
+      j.n_req = c.n_req;
+      j.pf_parents = P;
+      j.pf_tab = c.d_pftab.p;
+      j.pf_aoff = reinterpret_cast<const long long*>(c.d_pfaoff.p);
+      j.pf_meta = c.d_bmeta.p;
+    }
     if (pp.pipelined) {  // persistent: the CTAs loop over the tiles
       j.n_ctas = blocks;
       grid = std::min<int64_t>(blocks, (int64_t)c.n_sm * c.jit_occ[pp.jit_index]);
@@ -1646,6 +1698,22 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   c.tick("gather");
   Timer t(c, &c.st.ms_gather);
   const int64_t nreq = c.n_req;
+  if (c.proj_fused_active) {  // partials were written by the fused projected-leaf pass
+    const int threads = 256;
+    const int64_t xblocks = (nreq + threads - 1) / threads;
+    const double ar = c.kfinal[0][0], ai = c.kfinal[0][1], br = c.kfinal[1][0], bi = c.kfinal[1][1];
+    const double2 kf = make_double2(ar * br - ai * bi, ar * bi + ai * br);
+    // partials are in bucket order: fold them back to request order through breq
+    reduce_kernel<<<(unsigned)xblocks, threads, 0, c.stream>>>(reinterpret_cast<const double2*>(c.d_partial.p),
+                                                                (int)c.pf_rows, nreq, kf,
+                                                                reinterpret_cast<double2*>(c.d_acc.p),
+                                                                reinterpret_cast<const int32_t*>(c.d_breq.p));
+    launch_check("reduce_kernel", xblocks, threads, 0);
+    c.st.n_gather_launches += 1;
+    c.st.n_launches += 1;
+    c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
+    return;
+  }
   if (c.fused_active) {  // partials were written by the fused leaf pass
     const int threads = 256;
     const int64_t xblocks = (nreq + threads - 1) / threads;
@@ -1929,7 +1997,8 @@ static void plan_buffers_impl(Ctx& c, int64_t n_leaves);
 // can stall the host for milliseconds, so steady-state runs reuse the plan.
 static void plan_buffers(Ctx& c, int64_t n_leaves) {
   const std::vector<int64_t> key = {n_leaves, c.n_req, c.mem_budget_mb, (int64_t)c.sched_serial,
-                                    c.fused_active ? 1 : 0, c.group_log, c.grouped_leaf ? 1 : 0, c.max_chunk,
+                                    (c.fused_active ? 1 : 0) + (c.proj_fused_active ? 2 : 0), c.group_log,
+                                    c.grouped_leaf ? 1 : 0, c.max_chunk,
                                     c.host_only ? 1 : 0, c.overlap_gather};
   if (key == c.plan_key) return;
   plan_buffers_impl(c, n_leaves);
@@ -2014,7 +2083,9 @@ static void plan_buffers_impl(Ctx& c, int64_t n_leaves) {
 // counting sort on the device (histogram, CUB exclusive scan, scatter).
 static void build_buckets(Ctx& c) {
   const int D = (int)c.prog.levels.size() - 1;
-  const PassPlan& pp = c.prog.levels[D].passes[1].back();
+  // the bucketed side: B for the fused B gather; the grouped side of a fused projected pass
+  const int gside = c.proj_fused_active ? 1 - c.proj_side : 1;
+  const PassPlan& pp = c.prog.levels[D].passes[gside].back();
   BucketMap m{};
   m.n_g = (int)pp.gbits.size();
   m.n_l = pp.k;
@@ -2032,7 +2103,8 @@ static void build_buckets(Ctx& c) {
   CK(cudaMemsetAsync(cnt, 0, (size_t)(tiles + 1) * 4, c.stream));
   const unsigned blocks = (unsigned)std::max<int64_t>(1, (n + 255) / 256);
   if (n > 0)
-    bucket_count_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const int32_t*>(c.d_ib.p), n, m, cnt);
+    bucket_count_kernel<<<blocks, 256, 0, c.stream>>>(
+        reinterpret_cast<const int32_t*>(gside == 1 ? c.d_ib.p : c.d_ia.p), n, m, cnt);
   size_t tmp = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, tiles + 1, c.stream));
   c.d_cubtmp.ensure(std::max<size_t>(tmp, 16));
@@ -2040,9 +2112,16 @@ static void build_buckets(Ctx& c) {
   CK(cudaMemcpyAsync(cnt, start, (size_t)(tiles + 1) * 4, cudaMemcpyDeviceToDevice, c.stream));
   if (n > 0)
     bucket_fill_kernel<<<blocks, 256, 0, c.stream>>>(
-        reinterpret_cast<const int32_t*>(c.d_ib.p), reinterpret_cast<const int32_t*>(c.d_ia.p), n, m, cnt,
+        reinterpret_cast<const int32_t*>(gside == 1 ? c.d_ib.p : c.d_ia.p),
+        reinterpret_cast<const int32_t*>(gside == 1 ? c.d_ia.p : c.d_ib.p), n, m, cnt,
         reinterpret_cast<int32_t*>(c.d_breq.p), reinterpret_cast<int32_t*>(c.d_btl.p),
         reinterpret_cast<int32_t*>(c.d_bia.p));
+  if (c.proj_fused_active && n > 0) {
+    c.d_bmeta.ensure((size_t)n * sizeof(int2));
+    pf_meta_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const int32_t*>(c.d_bia.p),
+                                                 reinterpret_cast<const int32_t*>(c.d_btl.p), n,
+                                                 reinterpret_cast<int2*>(c.d_bmeta.p));
+  }
   CK(cudaGetLastError());
   c.bucket_valid = true;
 }
@@ -2054,13 +2133,14 @@ static void run_tree(Ctx& c) {
   int64_t n_leaves_bound = (int64_t)c.prefixes.size() * (c.branch_hi - c.branch_lo);
   plan_buffers(c, std::max<int64_t>(1, n_leaves_bound));
   c.st.n_levels = D + 1;
-  c.ovl = c.overlap_gather && c.grouped_leaf && !c.fused_active && !c.profile && !c.host_only && D >= 1;
+  c.ovl = c.overlap_gather && c.grouped_leaf && !c.fused_active && !c.proj_fused_active && !c.profile &&
+          !c.host_only && D >= 1;
   if (c.ovl && !c.gstream) {
     CK(cudaStreamCreateWithFlags(&c.gstream, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&c.ev_leaf, cudaEventDisableTiming));
     for (auto& e : c.ev_g) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  if (c.fused_active && !c.host_only && !c.bucket_valid && c.n_req > 0) {
+  if ((c.fused_active || c.proj_fused_active) && !c.host_only && !c.bucket_valid && c.n_req > 0) {
     finish_requests(c);
     build_buckets(c);
   }
@@ -2236,6 +2316,17 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "proj_perm") {
       c.proj_perm = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "proj_fuse") {
+      c.proj_fuse = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_u") {
+      if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "pf_u must be in [1, 8]");
+      c.pf_u = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_min_blocks") {
+      if (value < 0 || value > 4) throw GsError(GS_ERR_ARG, "pf_min_blocks must be in [0, 4]");
+      c.pf_min_blocks = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "proj_leaf") {
       c.proj_leaf = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -2389,7 +2480,8 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
       js += "]}";
     }
     js += "], \"tail\": [" + std::to_string(c.tail_ops[0].size()) + ", " + std::to_string(c.tail_ops[1].size()) +
-          "], \"proj_side\": " + std::to_string(c.proj_side) + ", \"proj_swaps\": " +
+          "], \"proj_side\": " + std::to_string(c.proj_side) + ", \"proj_fused\": " +
+          std::to_string(c.proj_fused_active ? 1 : 0) + ", \"proj_swaps\": " +
           std::to_string(c.proj_swaps.size()) + ", \"jit\": \"";
     for (char ch : c.jit_status) js += (ch == '"' || ch == '\\' || ch == '\n') ? ' ' : ch;
     js += "\"}";

@@ -43,6 +43,11 @@ struct JArgs {
   long long a_elems;
   long long n_ctas;   // logical tiles of a persistent (pipelined) pass kernel
   long long uni_p0;   // >= 0: the chunk is full fan-out -- parent = uni_p0 + slot / F, digits from slot % F
+  // projected-leaf fused pass (PassPlan::proj_fused): requests bucketed by this pass's tile
+  const void* pf_parents;     // projected side's parent states (level D-1), complex64
+  const void* pf_tab;         // float2 [group][8 << nk]: projected factor per sibling and request cross bits
+  const long long* pf_aoff;   // [group][8]: parent amplitude offset per sibling
+  const void* pf_meta;        // int2 per bucket slot: (tile-local index | cross bits << 16, parent base index)
 };
 
 struct JitModule;

@@ -923,4 +923,60 @@ static __global__ void bucket_fill_kernel(const int32_t* ib, const int32_t* ia, 
   bia[pos] = ia[i];
 }
 
+// Fused projected-leaf pass (jitgen::proj_fused_kernel), request side: per
+// bucket slot, the projected-side index with its leaf-level cross bits cleared
+// and the parent layout's bit swaps applied (abase), and the tile-local index
+// of the grouped side packed with the request's cross bits (tl | xc << 16).
+static __global__ void pf_meta_kernel(const int32_t* bia, const int32_t* btl, long long n, int2* meta) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long x = bia[i];
+  int xc = 0;
+  for (int k = 0; k < g_proj.n; ++k) {
+    xc |= (int)((x >> g_proj.s[k]) & 1) << k;
+    x &= ~(1LL << g_proj.s[k]);
+  }
+  for (int w = 0; w < g_proj.n_swap; ++w) {
+    const int a = g_proj.sa[w], b = g_proj.sb[w];
+    if (((x >> a) & 1) != ((x >> b) & 1)) x ^= (1LL << a) | (1LL << b);
+  }
+  meta[i] = make_int2(btl[i] | (xc << 16), (int)x);
+}
+
+// Fused projected-leaf pass, leaf side: per leaf group g (8 sibling slots) and
+// request cross bits xc, the projected factor c = w * prod_k a_k(d_k) U_k[xc_k, v_k(d_k)]
+// (complex64, as the leaf's own complex64 state would hold it) and, per slot,
+// the parent amplitude offset parent * p_elems + sum_k v_k(d_k) << abit_k.
+// Slots past n_states get c = 0.  One CTA per group, one thread per (xc, slot).
+static __global__ void pf_table_kernel(const unsigned long long* digits, const int32_t* parent,
+                                       const double* weights, long long n_states, long long p_elems,
+                                       float2* tab, long long* aoff) {
+  const int nk = g_proj.n, t = threadIdx.x;
+  if (t >= (8 << nk)) return;
+  const long long g = blockIdx.x;
+  const int s = t & 7, xc = t >> 3;  // table layout [group][xc][slot]: a request's 8 factors are contiguous
+  const long long slot = (g << 3) | s;
+  float2 c = make_float2(0.f, 0.f);
+  long long off = 0;
+  if (slot < n_states) {
+    const unsigned long long dg = digits[slot];
+    double pr = weights[slot], pi = 0.0;
+    off = (long long)parent[slot] * p_elems;
+    for (int k = 0; k < nk; ++k) {
+      const int d = (int)((dg >> (4 * k)) & 15ull);
+      const int vb = g_proj.v[k][d], xb = (xc >> k) & 1;
+      const double* u = g_proj.u[k] + 2 * (2 * xb + vb);
+      const double fr = g_proj.a[k][d][0] * u[0] - g_proj.a[k][d][1] * u[1];
+      const double fi = g_proj.a[k][d][0] * u[1] + g_proj.a[k][d][1] * u[0];
+      const double tr = pr * fr - pi * fi;
+      pi = pr * fi + pi * fr;
+      pr = tr;
+      off |= (long long)vb << g_proj.abit[k];
+    }
+    c = make_float2((float)pr, (float)pi);
+  }
+  tab[(g << (3 + nk)) + t] = c;
+  if (xc == 0) aoff[(g << 3) + s] = off;
+}
+
 }  // namespace gs

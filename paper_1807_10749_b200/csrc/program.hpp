@@ -62,6 +62,8 @@ struct PassPlan {
   int jit_index = -1;           // kernel gsj_<index> of the program's JIT module
   bool grouped_store = false;   // leaf level, last pass: grouped path-minor store
   bool fused_gather = false;    // leaf level, last B pass: gather instead of a B store (JIT)
+  bool proj_fused = false;      // leaf level, last pass of the grouped side: fused with the projected-side
+                                // gather (JIT; no leaf state of either side reaches HBM)
   bool pipelined = false;       // JIT: persistent kernel prefetching the next tile (option pipeline)
   int level = -1;               // path-tree level of the pass
   std::vector<int> store_perm;  // non-empty: state bit b is stored at address bit store_perm[b] (JIT only)

@@ -264,6 +264,8 @@ class Engine:
 
     def _check(self, code: int):
         if code != GS_OK:
+            if not getattr(self, "_h", None):
+                raise EngineError("engine context was released (ENGINES.release_others); get a fresh one")
             _raise(code, LIB.gs_last_error(self._h).decode())
 
     def set_option(self, key: str, value: int):
@@ -437,6 +439,34 @@ class _EngineCache:
             if eng is None:
                 eng = self.engines[key] = Engine(device, dtype)
             return eng
+
+    def release_others(self, keep: Engine) -> bool:
+        """Destroy this process's other idle engines on ``keep``'s device (each
+        sizes its path-tree buffers from the free HBM it saw, so a second
+        context can find too little).  True when any memory was released."""
+        freed = False
+        with self._lock:
+            for key, eng in list(self.engines.items()):
+                if eng is keep or eng.device != keep.device or not eng.lock.acquire(blocking=False):
+                    continue
+                try:
+                    eng.close()
+                    del self.engines[key]
+                    freed = True
+                finally:
+                    eng.lock.release()
+        return freed
+
+
+def run_with_memory_retry(eng: Engine, fn):
+    """``fn()``; on a device-memory shortfall, release the process's other idle
+    engines and try once more."""
+    try:
+        return fn()
+    except MemoryError:
+        if not ENGINES.release_others(eng):
+            raise
+        return fn()
 
 
 ENGINES = _EngineCache()

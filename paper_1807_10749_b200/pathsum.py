@@ -28,7 +28,7 @@ import numpy as np
 
 from .amplitudes import AmplitudeBatch
 from .circuit import Circuit
-from .engine import ENGINES
+from .engine import ENGINES, run_with_memory_retry
 from .lowering import lowered
 from .plan import SimPlan, path_digits
 
@@ -60,8 +60,9 @@ def _run(circuit, plan, requests, prefixes, branch_lo, branch_hi, device, dtype)
         eng.load_program(prog)
         # split_requests (pathsum.py:122-140) runs on the device, overlapped with the
         # first gate passes; IndexError as in the reference
-        res = eng.run_batched(idx, circuit.n_qubits, plan.cut.block_a, plan.cut.block_b, plan.x_p,
-                              prefixes, branch_lo, branch_hi)
+        res = run_with_memory_retry(eng, lambda: eng.run_batched(
+            idx, circuit.n_qubits, plan.cut.block_a, plan.cut.block_b, plan.x_p, prefixes, branch_lo,
+            branch_hi))
     return AmplitudeBatch(idx, res.amps)
 
 

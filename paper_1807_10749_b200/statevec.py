@@ -69,7 +69,7 @@ def run_full(
     dtype="c64",
 ) -> StateBlock:
     """Simulate the full circuit from |0...0> on the GPU (reference ``run_full``)."""
-    from .engine import ENGINES, precision_code
+    from .engine import ENGINES, precision_code, run_with_memory_retry
 
     n = circuit.n_qubits
     precision_code(dtype)  # ValueError for an unknown dtype, before any work
@@ -82,7 +82,7 @@ def run_full(
     eng = ENGINES.get(device, dtype)
     with eng.lock:
         eng.load_program(lowered(circuit, full_cut(circuit)))
-        return StateBlock(n, eng.run_full().amps)
+        return StateBlock(n, run_with_memory_retry(eng, eng.run_full).amps)
 
 
 def fetch_amplitudes(state: StateBlock, indices) -> AmplitudeBatch:

@@ -130,7 +130,7 @@ def _device_worker(rank, world, port, name, window, out_dir):
     circ, plan, req, _ = configs.build(name)
     pre = plan.retained[:window]
     plain = run_batched_sharded(circ, plan, req, prefixes=pre, device=0, dst=None)
-    repro = run_batched_sharded(circ, plan, req, prefixes=pre, device=0, reproducible=True)
+    repro = run_batched_sharded(circ, plan, req, prefixes=pre, device=0, dst=None, reproducible=True)
     np.save(os.path.join(out_dir, f"plain{rank}.npy"), plain.amps)
     np.save(os.path.join(out_dir, f"repro{rank}.npy"), repro.amps)
     dist.barrier()

@@ -598,3 +598,41 @@ def test_overlapped_gathers_bitwise(ps, name):
             eng.set_option("max_chunk", 1 << 20)
     for a, b in zip(got[0], got[1]):
         assert np.array_equal(a, b) and np.abs(a).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg4v2", "cfg3v2"])
+def test_fused_projected_leaf_pass(ps, name):
+    """proj_fuse=1 (default): the grouped side's last leaf pass does the
+    projected-side gather itself (no leaf state reaches HBM).  Equal to the
+    separate leaf pass + projected gather (proj_fuse=0) to complex64 rounding of
+    the projected amplitudes, for each epilogue unroll, partial last groups,
+    branch sub-ranges and duplicate prefixes; and to the reference window."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=20000)
+    eng = _engine("c64")
+    got = {}
+    try:
+        for key, opts in (("sep", {"proj_fuse": 0}), ("fused", {}), ("u1", {"pf_u": 1}),
+                          ("u4", {"pf_u": 4, "pf_min_blocks": 0})):
+            for k, v in opts.items():
+                eng.set_option(k, v)
+            eng.load_program(lowered(circ, plan.cut))
+            assert eng.describe()["proj_fused"] == (0 if key == "sep" else 1)
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[key] = (eng.run(plan.x_p, pre[:9], 0, plan.branch_space).amps,
+                        eng.run(plan.x_p, pre[:5], 1, plan.branch_space - 1).amps,
+                        eng.run(plan.x_p, np.concatenate([pre[:3], pre[:3]]), 0, plan.branch_space).amps)
+            for k in opts:
+                eng.set_option(k, {"proj_fuse": 1, "pf_u": 2, "pf_min_blocks": 3}[k])
+    finally:
+        for k, v in (("proj_fuse", 1), ("pf_u", 2), ("pf_min_blocks", 3)):
+            eng.set_option(k, v)
+    for key in ("fused", "u1", "u4"):
+        for a, b in zip(got["sep"], got[key]):
+            assert np.abs(a).max() > 0
+            assert rel_l2(b, a) <= 2e-6, key
+    g = load_amps(name) if name != "cfg4v2" else None
+    if g is not None:
+        got = ps.run_batched(circ, plan, g["requests"], prefixes=g["prefixes"]).amps
+        assert rel_l2(got, g["amps_c64"]) <= C64_TOL
