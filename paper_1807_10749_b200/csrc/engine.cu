@@ -2117,7 +2117,10 @@ static void build_buckets(Ctx& c) {
         reinterpret_cast<int32_t*>(c.d_breq.p), reinterpret_cast<int32_t*>(c.d_btl.p),
         reinterpret_cast<int32_t*>(c.d_bia.p));
   if (c.proj_fused_active && n > 0) {
-    c.d_bmeta.ensure((size_t)n * sizeof(int2));
+    // the fused pass reads whole 32-slot warp rows past the last bucket: zero padding
+    // makes those rows address element 0 of the parent (their results are not written)
+    c.d_bmeta.ensure((size_t)(n + 64) * sizeof(int2));
+    CK(cudaMemsetAsync(reinterpret_cast<int2*>(c.d_bmeta.p) + n, 0, 64 * sizeof(int2), c.stream));
     pf_meta_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const int32_t*>(c.d_bia.p),
                                                  reinterpret_cast<const int32_t*>(c.d_btl.p), n,
                                                  reinterpret_cast<int2*>(c.d_bmeta.p));
