@@ -54,7 +54,34 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-procs", type=int, default=0)
     ap.add_argument("--opt", action="append", default=[], help="engine option key=value")
+    ap.add_argument("--describe-out", default="", help="write gs_describe() + schedule hash here")
+    ap.add_argument("--whole-job", action="store_true",
+                    help="time the config's whole retained set in one public-API call (e2e, host buffers)")
+    ap.add_argument("--no-single-core", action="store_true", help="skip the single-core CPU leg")
     return ap.parse_args()
+
+
+def schedule_hash(desc: dict, window: int, n_req: int) -> str:
+    """Key of the exact schedule being timed (the pass plan, leaf handling, window
+    and request count); profiles/traffic.json holds ncu DRAM bytes per key."""
+    import hashlib
+
+    d = {k: v for k, v in desc.items() if k != "jit"}  # the jit field carries compile timings
+    blob = json.dumps(d, sort_keys=True) + f"|{window}|{n_req}"
+    return hashlib.sha256(blob.encode()).hexdigest()[:16]
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 DEFAULT_WINDOW = {"cfg1": 16, "cfg1v2": 32, "cfg2": 32768, "cfg2v2": 32768, "cfg2h": 2048,
@@ -205,10 +232,52 @@ def dist_setup(args):
     return world, rank, local
 
 
+def main_whole_job(args):
+    """The config's whole retained set in ONE public-API call (host requests in,
+    host amplitudes out), timed by the host clock around the call; the device-side
+    time of the same job is the engine's event time (stats ms_total)."""
+    import torch
+
+    from paper_1807_10749_b200 import configs
+    from paper_1807_10749_b200.engine import ENGINES
+    from paper_1807_10749_b200.pathsum import run_batched
+
+    torch.cuda.set_device(0)
+    name = args.config
+    circ, plan, req, pre_all = configs.build(name)
+    eng = ENGINES.get(0, args.dtype)
+    for kv in args.opt:
+        key, val = kv.split("=")
+        eng.set_option(key, int(val))
+    run_batched(circ, plan, req, prefixes=pre_all[:64])  # untimed: program load, JIT, buffers
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = run_batched(circ, plan, req, prefixes=pre_all)
+    wall = time.perf_counter() - t0
+    paths = int(pre_all.size) * plan.branch_space
+    line = {
+        "metric": METRIC, "value": paths / wall, "unit": "paths/s", "n_gpus": 1, "steps": 1, "warmup": 1,
+        "ms_per_step": 1e3 * wall, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c64 (fp32 complex states, fp64 accumulation)" if args.dtype == "c64" else "c128",
+        "data": "synthetic: reference-generator circuit (seed 0), challenge_indices(seed 12345)",
+        "config": {"workload": f"{name} whole job: all {pre_all.size} retained prefixes x {plan.branch_space} "
+                               f"branches = {paths} paths, {req.size} bitstrings, one run_batched call",
+                   "timer": "host wall clock around the public call (request upload, path tree, result "
+                            "download into host memory)"},
+        "e2e": {"value": paths / wall, "unit": "paths/s", "h2d_bytes_per_step": int(8 * req.size),
+                "d2h_bytes_per_step": int(16 * req.size)},
+        "amplitude_norm2": float(np.vdot(res.amps, res.amps).real),
+        "whole_job_seconds": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return main_reference(args)
+    if args.whole_job:
+        return main_whole_job(args)
 
     import torch
     import torch.distributed as dist
@@ -339,7 +408,9 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (the specialised gate passes) from the profiled step
+    # roofline of the dominant kernel class, from the profiled step (CUDA events on the
+    # engine's stream around every level): the gate passes above the leaf level (HBM
+    # streaming) and the leaf level (the fused projected-leaf pass where it applies)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -347,42 +418,62 @@ def main():
     except OSError:
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
-    ms_pass = prof["ms_pass"]
-    launches = max(1, prof["n_pass_launches"])
-    traffic = None  # measured DRAM bytes per pass launch (ncu launch list committed under profiles/)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    desc = eng.describe()
+    shash = schedule_hash(desc, window, n_req)
+    if args.describe_out:
+        with open(args.describe_out, "w") as fh:
+            json.dump(dict(desc, schedule_hash=shash, config=name, window=window, n_req=n_req), fh)
+    traffic_rec = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tr = json.load(fh).get(name)
-        if tr and args.window == 0:
-            traffic = tr["pass_dram_bytes_per_launch"]
-    except (OSError, ValueError, KeyError):
+            traffic_rec = json.load(fh).get(shash)
+    except (OSError, ValueError):
         pass
-    roofline = {
-        "bound": "hbm",
-        "kernel": "gsj_* (load-time specialised gate passes)" if "jit:" in eng.describe()["jit"]
-                  else "pass2_kernel",
-        "achieved": prof["pass_bytes_min"] / (ms_pass / 1e3) / 1e9 if ms_pass else None,
-        "peak": peak,
-        "unit": "GB/s",
-        "frac": (prof["pass_bytes_min"] / (ms_pass / 1e3) / 1e9) / peak if ms_pass else None,
-        "traffic": traffic,
-        "traffic_note": "DRAM read+write bytes per pass launch from profiles/traffic.json (ncu launch list "
-                        "of this config); below the algorithmic bytes where sibling nodes share their "
-                        "parent's tiles in L1/L2 (the algorithmic count reads the parent once per child, so "
-                        "frac can exceed 1; dram_frac is the measured-DRAM fraction)",
-        "dram_achieved": (traffic / (ms_pass / launches / 1e3) / 1e9) if (traffic and ms_pass) else None,
-        "dram_frac": (traffic / (ms_pass / launches / 1e3) / 1e9 / peak) if (traffic and ms_pass) else None,
-        "algorithmic_bytes_per_launch": prof["pass_bytes_min"] / launches,
-        "avg_launch_ms": ms_pass / launches,
-        "kernel_bytes_per_launch": prof["pass_bytes"] / launches,
-        "kernel_gbs": prof["pass_bytes"] / (ms_pass / 1e3) / 1e9 if ms_pass else None,
-        "share_of_step": ms_pass / prof["ms_total"] if prof["ms_total"] else None,
-        "gather_ms": prof["ms_gather"],
-        "peak_source": peak_src,
-        "basis": "algorithmic = one read+write of both half-states per path-tree node per level "
-                 "(SURVEY.md §8d); kernel_gbs counts every pass actually made",
-    }
+    if traffic_rec is None:
+        print(f"bench: no ncu DRAM capture for schedule {shash} in profiles/traffic.json; "
+              f"roofline.traffic is null (tools/round_prof.sh records it)", file=sys.stderr)
+    fused = bool(desc.get("proj_fused"))
+    classes = {}
+    ms_leaf = prof["ms_leaf"]
+    n_leaf = max(0, prof["n_leaf_launches"])
+    for cls, ms_c, by_c, n_c, kern in (
+            ("upper_passes", prof["ms_pass"] - ms_leaf, prof["upper_bytes_alg"],
+             prof["n_pass_launches"] - n_leaf, "gsj_* gate passes above the leaf level"),
+            ("leaf", ms_leaf, prof["leaf_bytes_alg"], n_leaf,
+             "gsj_* fused projected-leaf pass (leaf gates + projected gather)" if fused
+             else "gsj_* leaf-level passes")):
+        if n_c <= 0 or ms_c <= 0:
+            continue
+        per_launch_ms = ms_c / n_c
+        ach = by_c / (ms_c / 1e3) / 1e9
+        tr = (traffic_rec or {}).get(cls)
+        classes[cls] = {
+            "bound": "hbm", "kernel": kern, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": tr["dram_bytes_per_launch"] if tr else None,
+            "traffic_vs_algorithmic": (tr["dram_bytes_per_launch"] / (by_c / n_c)) if tr and by_c else None,
+            "algorithmic_bytes_per_launch": by_c / n_c, "avg_launch_ms": per_launch_ms, "launches": n_c,
+            "share_of_step": ms_c / prof["ms_total"] if prof["ms_total"] else None,
+        }
+    if prof["ms_gather"] > 0:
+        classes["gather"] = {"kernel": "reduce_kernel (fold of the fused pass's partials)" if fused
+                             else "leaf gather + reduce", "ms": prof["ms_gather"],
+                             "algorithmic_bytes": prof["gather_bytes"],
+                             "achieved": prof["gather_bytes"] / (prof["ms_gather"] / 1e3) / 1e9,
+                             "share_of_step": prof["ms_gather"] / prof["ms_total"] if prof["ms_total"] else None}
+    dom = max((c for c in ("upper_passes", "leaf") if c in classes),
+              key=lambda c: classes[c]["avg_launch_ms"] * classes[c]["launches"], default=None)
+    roofline = dict(classes[dom]) if dom else {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
+                                               "frac": None, "traffic": None}
+    roofline.update({
+        "class": dom, "peak_source": peak_src, "schedule_hash": shash,
+        "traffic_source": (traffic_rec or {}).get("source"),
+        "basis": "algorithmic bytes the schedule must move per launch: every parent state read once per "
+                 "level chunk, every written state written once (later passes of a level read+write their "
+                 "node); the fused leaf pass reads each parent once per side and writes one fp64 partial "
+                 "per (request, 8-leaf group) -- no leaf state reaches HBM",
+        "classes": classes,
+    })
     line = {
         "metric": METRIC,
         "value": value,
@@ -404,6 +495,7 @@ def main():
         },
         "e2e": e2e,
         "roofline": roofline,
+        "schedule_hash": shash,
         "gpu_launches": int(sum(st["n_launches"] for st in stats)),
         "clocks": clk.summary(),
         "nodes_per_step": int(np.mean([st["n_nodes"] for st in stats])),
@@ -418,23 +510,53 @@ def main():
         cpu_paths = sample.size * plan.branch_space
         line["cpu_baseline"] = {
             "value": cpu_paths / wall, "unit": "paths/s", "cores": used, "kind": "port",
+            "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
             "sample": f"{sample.size} prefixes x {plan.branch_space} branches of the same window, "
                       f"{used} forked processes, numpy restatement of reference run_batched",
         }
+        if not args.no_single_core:  # one process, one thread: the reference's own per-core rate
+            w1, _, _ = cpu_reference(name, sample[:1], n_req, 1)
+            line["cpu_baseline"]["single_core"] = {
+                "value": plan.branch_space / w1, "unit": "paths/s", "cores": 1,
+                "sample": f"1 prefix x {plan.branch_space} branches, 1 process (OMP_NUM_THREADS=1)"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def main_reference(args):
-    """Reference arm: the reference algorithm (oracle port of run_batched) on all host cores.
+def _ref_job(args):
+    """One CPU process of the reference arm: the reference package's own
+    run_batched (gridsim, from baseline/_ref) over a slice of prefixes."""
+    name, prefixes, n_req = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from paper_1807_10749_b200 import configs
+    from paper_1807_10749_b200.gridsim_engine import load_gridsim
 
+    gc, gps = load_gridsim("circuit"), load_gridsim("pathsum")
+    circ, plan, req, _ = configs.build(name, n_req=n_req)
+    spec = configs.CONFIGS[name]
+    with open(spec.circuit_file) as fh:
+        rc = gc.parse_circuit(fh.read(), spec.rows, spec.cols)
+    cut = gc.Cut(plan.cut.orientation, plan.cut.position, tuple(plan.cut.block_a), tuple(plan.cut.block_b))
+    rplan = gps.SimPlan(cut, plan.fidelity, tuple(plan.radices), plan.x_p, plan.x_b, plan.d_p, plan.d_b,
+                        plan.seed, plan.retained)
+    t = time.perf_counter()
+    amps = gps.run_batched(rc, rplan, req, prefixes=np.asarray(prefixes, dtype=np.int64)).amps
+    return time.perf_counter() - t, amps
+
+
+def main_reference(args):
+    """Reference arm: the reference's CPU implementation of the path on all host cores.
+
+    Where the reference package is installed (baseline/_ref, `gridsim`), each
+    process runs its own ``gridsim.pathsum.run_batched`` (kind "reference");
+    otherwise the numpy restatement in oracle/ (kind "port", bit-exact with it).
     A timed step is the workload's natural unit on every core: each process
     evaluates one retained prefix with all of its branches (the reference's
     per-prefix job, orchestrator.py:133-159, on its batched engine).  Warm-up
-    steps only import and run one path on one process (they are untimed).
-    Rank 0 alone runs under torchrun.
+    steps only import and run small jobs (untimed).  Rank 0 alone runs under
+    torchrun.
     """
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -443,22 +565,29 @@ def main_reference(args):
     import multiprocessing as mp
 
     from paper_1807_10749_b200 import configs
+    from paper_1807_10749_b200.gridsim_engine import gridsim_available
 
     name = args.config
     circ, plan, req, pre_all = configs.build(name)
+    kind = "reference" if gridsim_available() else "port"
+    job = _ref_job if kind == "reference" else _cpu_job
     procs = args.cpu_procs or min(os.cpu_count() or 1, 64)
     pool = mp.get_context("fork").Pool(procs)
     for s in range(args.warmup):
-        pool.map(_cpu_job, [(name, pre_all[s:s + 1], 64)])
+        pool.map(job, [(name, pre_all[s:s + 1], 64)] * procs)
     times, paths = [], 0
     for s in range(args.steps):
         sample = pre_all[(s * procs) % max(1, pre_all.size - procs):][:procs]
-        wall, _, used = cpu_reference(name, sample, req.size, procs, pool)
-        times.append(wall)
+        slices = [x for x in np.array_split(sample, procs) if x.size]
+        t = time.perf_counter()
+        pool.map(job, [(name, x, req.size) for x in slices])
+        times.append(time.perf_counter() - t)
         paths += sample.size * plan.branch_space
     pool.close()
     total = sum(times)
     value = paths / total
+    what = ("gridsim.pathsum.run_batched (the reference package, baseline/_ref)" if kind == "reference"
+            else "numpy restatement of reference run_batched (oracle/)")
     line = {
         "metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
@@ -467,9 +596,9 @@ def main_reference(args):
         "data": "synthetic: reference-generator circuit (seed 0), challenge_indices(seed 12345)",
         "config": {"workload": describe(name, plan, procs, req.size) + " (CPU: one prefix per process)",
                    "parallelism": f"{procs} forked CPU processes"},
-        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": procs, "kind": "port",
-                         "sample": f"{procs} prefixes x {plan.branch_space} branches per step "
-                                   f"(numpy restatement of reference run_batched, oracle/)"},
+        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": procs, "kind": kind,
+                         "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+                         "sample": f"{procs} prefixes x {plan.branch_space} branches per step, {what}"},
         "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 
 /* error codes; the Python binding maps them onto the reference's exceptions */
 #define GS_OK 0
@@ -83,6 +83,14 @@ typedef struct gs_stats {
   double d2h_bytes;          /* device->host bytes copied by this gs_run     */
   double host_ms_enqueue;    /* host time to plan + enqueue the whole run    */
   double host_ms_max_gap;    /* longest host interval between two launches   */
+  /* roofline basis of the two kernel classes (appended in ABI 2) */
+  double ms_leaf;            /* leaf-level pass time incl. a fused gather (profile only), part of ms_pass */
+  double upper_bytes_alg;    /* gate passes above the leaf level: each parent state read once per
+                                level chunk (first pass), every written state once, later passes
+                                read+write their node                                            */
+  double leaf_bytes_alg;     /* leaf level: parents read once per side, leaf states written and
+                                gathered (separate gather) or fp64 partials written (fused)      */
+  int64_t n_leaf_launches;   /* leaf-level pass launches                                        */
 } gs_stats;
 
 int gs_abi_version(void);

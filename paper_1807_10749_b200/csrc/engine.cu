@@ -272,9 +272,12 @@ struct Ctx {
   int sink_ops = 12;          // option: move a level's trailing pass of <= sink_ops ops into the next level
   int gather_gpy = 0;         // option: leaf groups per gather y-block (0 = auto)
   int proj_side = -1;         // leaf side evaluated by projection (no leaf passes), -1 none
+  int tile_major = 0;         // option: JIT passes above the leaf level launch their CTAs tile-major (siblings
+                              // of one tile back to back: a parent tile is read from DRAM once)
   int proj_fuse = 1;          // option: fuse the other side's last leaf pass with the projected gather (JIT)
   int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
+  int pf_tail = 1;            // option: the fused pass's last one-qubit-op stage runs per request in its epilogue
   bool proj_fused_active = false;  // the fused projected-leaf pass is compiled for the loaded program
   int64_t pf_rows = 0;        // partial rows written by the current leaf chunk's fused pass
   DevBuf d_proj;              // device copy of ProjProgD for the fused pass
@@ -1569,7 +1572,7 @@ struct Timer {
   double* acc;
   cudaEvent_t a = nullptr, b = nullptr;
   Timer(Ctx& cc, double* ac) : c(cc), acc(ac) {
-    if (c.profile && !c.host_only) {
+    if (acc && c.profile && !c.host_only) {
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       cudaEventRecord(a, c.stream);
@@ -1591,9 +1594,28 @@ struct Timer {
 template <typename R>
 static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const void* src_b,
                              void* dst_a, void* dst_b, const int32_t* parent,
-                             const uint64_t* digit, bool root) {
+                             const uint64_t* digit, bool root, int64_t n_parents = 1) {
   Timer t(c, &c.st.ms_pass);
   const Level& L = c.prog.levels[l];
+  const int D = (int)c.prog.levels.size() - 1;
+  Timer tl(c, l == D ? &c.st.ms_leaf : nullptr);
+  // roofline basis: what these passes must move (parents read once, states written once)
+  for (int side = 0; side < 2; ++side) {
+    const double sb = (double)(1LL << c.prog.q[side]) * (double)c.esize();
+    if (c.prog.q[side] == 0 || (l == D && side == c.proj_side)) {
+      if (l == D && side == c.proj_side) c.st.leaf_bytes_alg += (double)n_parents * sb;  // parents, read once
+      continue;
+    }
+    double b = 0;
+    for (size_t i = 0; i < L.passes[side].size(); ++i) {
+      const PassPlan& pp = L.passes[side][i];
+      const double rd = i == 0 ? (root ? 0.0 : (double)n_parents * sb) : (double)n * sb;
+      const double wr = (pp.proj_fused && c.proj_fused_active) ? 0.0 : (double)n * sb;
+      b += rd + wr;
+      if (l == D) c.st.n_leaf_launches++;
+    }
+    (l == D ? c.st.leaf_bytes_alg : c.st.upper_bytes_alg) += b;
+  }
   const void* srcs[2] = {src_a, src_b};
   void* dsts[2] = {dst_a, dst_b};
   for (int side = 0; side < 2; ++side) {
@@ -1711,7 +1733,9 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     launch_check("reduce_kernel", xblocks, threads, 0);
     c.st.n_gather_launches += 1;
     c.st.n_launches += 1;
-    c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
+    // the fused pass wrote one fp64 partial per (request, leaf group); the fold reads them once
+    c.st.leaf_bytes_alg += 16.0 * (double)c.pf_rows * (double)nreq;
+    c.st.gather_bytes += 16.0 * (double)c.pf_rows * (double)nreq + 32.0 * nreq;
     return;
   }
   if (c.fused_active) {  // partials were written by the fused leaf pass
@@ -1861,7 +1885,10 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   launch_check("reduce_kernel", xblocks, threads, 0);
   c.st.n_gather_launches += 2;
   c.st.n_launches += 2;
-  c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
+  if (c.grouped_leaf && c.proj_side >= 0)  // per request and 8-leaf group: one 64-byte leaf run + a parent pair
+    c.st.gather_bytes += (double)((n + 7) / 8) * (double)nreq * (8.0 * c.esize() + 2.0 * c.esize()) + 32.0 * nreq;
+  else
+    c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
 }
 
 template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int64_t n_nodes) {
@@ -1973,8 +2000,10 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
       CK(cudaStreamWaitEvent(c.stream, c.ev_g[0], 0));
       CK(cudaStreamWaitEvent(c.stream, c.ev_g[1], 0));
     }
+    int64_t n_par = n > 0 ? 1 : 0;  // distinct parents of the chunk (children come in parent order)
+    for (int64_t j = 1; j < n; ++j) n_par += chunk[j].parent != chunk[j - 1].parent;
     run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
-                        at(c.lvl_b, l + 1), d_parent, d_digit, false);
+                        at(c.lvl_b, l + 1), d_parent, d_digit, false, n_par);
     c.uni_p0 = -1;
     if (f >= 0) {
       CK(cudaEventRecord(c.ev_leaf, c.stream));
@@ -2319,12 +2348,18 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "proj_perm") {
       c.proj_perm = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "tile_major") {
+      c.tile_major = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "proj_fuse") {
       c.proj_fuse = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_u") {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "pf_u must be in [1, 8]");
       c.pf_u = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_tail") {
+      c.pf_tail = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_min_blocks") {
       if (value < 0 || value > 4) throw GsError(GS_ERR_ARG, "pf_min_blocks must be in [0, 4]");

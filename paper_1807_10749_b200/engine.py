@@ -71,6 +71,10 @@ class GsStats(ctypes.Structure):
         ("d2h_bytes", ctypes.c_double),
         ("host_ms_enqueue", ctypes.c_double),
         ("host_ms_max_gap", ctypes.c_double),
+        ("ms_leaf", ctypes.c_double),
+        ("upper_bytes_alg", ctypes.c_double),
+        ("leaf_bytes_alg", ctypes.c_double),
+        ("n_leaf_launches", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -120,7 +124,7 @@ def _load():
     lib.gs_host_alloc.argtypes = [ctypes.c_int64, ctypes.POINTER(_P)]
     lib.gs_host_free.argtypes = [_P]
     lib.gs_host_free.restype = None
-    if lib.gs_abi_version() != 1:
+    if lib.gs_abi_version() != 2:
         raise ImportError("libgridsim_b200.so ABI version mismatch")
     return lib
 

@@ -114,6 +114,13 @@ def _device_functions(sv):
             "run_prefix_tree": run_prefix_tree, "run_path": run_path, "run_full": run_full}
 
 
+def run_approx_b200(circuit, plan, requests, skip_zeros: bool = True, **kw):
+    """``run_approx`` on the B200 for ``gridsim`` objects, returning
+    ``gridsim.statevec.AmplitudeBatch`` (the function the reference's
+    ``engine="b200"`` branch calls)."""
+    return _device_functions(load_gridsim("statevec"))["run_approx"](circuit, plan, requests, skip_zeros, **kw)
+
+
 def install(default: bool = False) -> None:
     """Register ``engine="b200"`` in ``gridsim`` (see the module docstring).
 

@@ -22,7 +22,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(engine.EXPORTED_SYMBOLS)
     for name in declared:
         assert hasattr(engine.LIB, name), name
-    assert engine.LIB.gs_abi_version() == 1
+    assert engine.LIB.gs_abi_version() == 2
 
 
 def host_engine(dtype="c64"):

@@ -308,14 +308,18 @@ def test_pipelined_pass_kernels_bitwise(ps, name):
     branch_hi = 2 if name == "cfg5" else plan.branch_space
     eng = _engine("c64")
     got = {}
-    for pipe in (0, 1):
-        eng.set_option("pipeline", pipe)
-        try:
-            eng.load_program(lowered(circ, plan.cut))
-            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
-            got[pipe] = eng.run(plan.x_p, window, 0, branch_hi).amps
-        finally:
-            eng.set_option("pipeline", 0)
+    eng.set_option("proj_fuse", 0)  # the same leaf path both times (the fused pass is never pipelined)
+    try:
+        for pipe in (0, 1):
+            eng.set_option("pipeline", pipe)
+            try:
+                eng.load_program(lowered(circ, plan.cut))
+                eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+                got[pipe] = eng.run(plan.x_p, window, 0, branch_hi).amps
+            finally:
+                eng.set_option("pipeline", 0)
+    finally:
+        eng.set_option("proj_fuse", 1)
     assert np.array_equal(got[0], got[1])
     assert np.abs(got[1]).max() > 0
 
@@ -612,9 +616,10 @@ def test_fused_projected_leaf_pass(ps, name):
     circ, plan, req, pre = configs.build(name, n_req=20000)
     eng = _engine("c64")
     got = {}
+    DEFAULTS = {"proj_fuse": 1, "pf_tail": 1, "pf_min_blocks": 3, "tile_major": 0}
     try:
-        for key, opts in (("sep", {"proj_fuse": 0}), ("fused", {}), ("u1", {"pf_u": 1}),
-                          ("u4", {"pf_u": 4, "pf_min_blocks": 0})):
+        for key, opts in (("sep", {"proj_fuse": 0}), ("fused", {}), ("notail", {"pf_tail": 0}),
+                          ("mb0", {"pf_min_blocks": 0}), ("tilemajor", {"tile_major": 1})):
             for k, v in opts.items():
                 eng.set_option(k, v)
             eng.load_program(lowered(circ, plan.cut))
@@ -624,11 +629,11 @@ def test_fused_projected_leaf_pass(ps, name):
                         eng.run(plan.x_p, pre[:5], 1, plan.branch_space - 1).amps,
                         eng.run(plan.x_p, np.concatenate([pre[:3], pre[:3]]), 0, plan.branch_space).amps)
             for k in opts:
-                eng.set_option(k, {"proj_fuse": 1, "pf_u": 2, "pf_min_blocks": 3}[k])
+                eng.set_option(k, DEFAULTS[k])
     finally:
-        for k, v in (("proj_fuse", 1), ("pf_u", 2), ("pf_min_blocks", 3)):
+        for k, v in DEFAULTS.items():
             eng.set_option(k, v)
-    for key in ("fused", "u1", "u4"):
+    for key in ("fused", "notail", "mb0", "tilemajor"):
         for a, b in zip(got["sep"], got[key]):
             assert np.abs(a).max() > 0
             assert rel_l2(b, a) <= 2e-6, key
