@@ -272,12 +272,14 @@ struct Ctx {
   int sink_ops = 12;          // option: move a level's trailing pass of <= sink_ops ops into the next level
   int gather_gpy = 0;         // option: leaf groups per gather y-block (0 = auto)
   int proj_side = -1;         // leaf side evaluated by projection (no leaf passes), -1 none
-  int tile_major = 0;         // option: JIT passes above the leaf level launch their CTAs tile-major (siblings
-                              // of one tile back to back: a parent tile is read from DRAM once)
+  int tile_major = 2;         // option: JIT passes of levels >= 1 launch their CTAs tile-major (siblings of one
+                              // tile back to back: a parent tile is read from DRAM once); 2 = auto (>= 2^24
+                              // amplitudes: cfg5 +1%, cfg4 -1% when forced on)
   int proj_fuse = 1;          // option: fuse the other side's last leaf pass with the projected gather (JIT)
   int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
-  int pf_tail = 1;            // option: the fused pass's last one-qubit-op stage runs per request in its epilogue
+  int pf_tail = 0;            // option: the fused pass's last one-qubit-op stage runs per request in its epilogue
+                              // (measured: cfg4 -1.3%, cfg4v2 +2%, cfg3v2 equal; off)
   bool proj_fused_active = false;  // the fused projected-leaf pass is compiled for the loaded program
   int64_t pf_rows = 0;        // partial rows written by the current leaf chunk's fused pass
   DevBuf d_proj;              // device copy of ProjProgD for the fused pass
@@ -2349,7 +2351,8 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       c.proj_perm = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "tile_major") {
-      c.tile_major = value ? 1 : 0;
+      if (value < 0 || value > 2) throw GsError(GS_ERR_ARG, "tile_major must be 0, 1 or 2");
+      c.tile_major = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "proj_fuse") {
       c.proj_fuse = value ? 1 : 0;
@@ -2519,7 +2522,10 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
     }
     js += "], \"tail\": [" + std::to_string(c.tail_ops[0].size()) + ", " + std::to_string(c.tail_ops[1].size()) +
           "], \"proj_side\": " + std::to_string(c.proj_side) + ", \"proj_fused\": " +
-          std::to_string(c.proj_fused_active ? 1 : 0) + ", \"proj_swaps\": " +
+          std::to_string(c.proj_fused_active ? 1 : 0) + ", \"opts\": {\"pf_tail\": " + std::to_string(c.pf_tail) +
+          ", \"tile_major\": " + std::to_string(c.tile_major) + ", \"pf_min_blocks\": " +
+          std::to_string(c.pf_min_blocks) + ", \"pipeline\": " + std::to_string(c.pipeline) + ", \"sink_ops\": " +
+          std::to_string(c.sink_ops) + ", \"reg_bits\": " + std::to_string(c.reg_bits) + "}, \"proj_swaps\": " +
           std::to_string(c.proj_swaps.size()) + ", \"jit\": \"";
     for (char ch : c.jit_status) js += (ch == '"' || ch == '\\' || ch == '\n') ? ' ' : ch;
     js += "\"}";

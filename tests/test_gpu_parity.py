@@ -616,9 +616,9 @@ def test_fused_projected_leaf_pass(ps, name):
     circ, plan, req, pre = configs.build(name, n_req=20000)
     eng = _engine("c64")
     got = {}
-    DEFAULTS = {"proj_fuse": 1, "pf_tail": 1, "pf_min_blocks": 3, "tile_major": 0}
+    DEFAULTS = {"proj_fuse": 1, "pf_tail": 0, "pf_min_blocks": 3, "tile_major": 2}
     try:
-        for key, opts in (("sep", {"proj_fuse": 0}), ("fused", {}), ("notail", {"pf_tail": 0}),
+        for key, opts in (("sep", {"proj_fuse": 0}), ("fused", {}), ("tail", {"pf_tail": 1}),
                           ("mb0", {"pf_min_blocks": 0}), ("tilemajor", {"tile_major": 1})):
             for k, v in opts.items():
                 eng.set_option(k, v)
@@ -633,7 +633,7 @@ def test_fused_projected_leaf_pass(ps, name):
     finally:
         for k, v in DEFAULTS.items():
             eng.set_option(k, v)
-    for key in ("fused", "notail", "mb0", "tilemajor"):
+    for key in ("fused", "tail", "mb0", "tilemajor"):
         for a, b in zip(got["sep"], got[key]):
             assert np.abs(a).max() > 0
             assert rel_l2(b, a) <= 2e-6, key
@@ -641,3 +641,24 @@ def test_fused_projected_leaf_pass(ps, name):
     if g is not None:
         got = ps.run_batched(circ, plan, g["requests"], prefixes=g["prefixes"]).amps
         assert rel_l2(got, g["amps_c64"]) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+def test_tile_major_cta_order_bitwise(ps, name):
+    """tile_major (CTA launch order of the passes below the root) changes only which
+    CTA runs when: bitwise equal sums."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    circ, plan, req, pre = configs.build(name, n_req=4096)
+    window = pre[:2] if name == "cfg5" else pre[:8]
+    eng = _engine("c64")
+    got = {}
+    try:
+        for tm in (0, 1):
+            eng.set_option("tile_major", tm)
+            eng.load_program(lowered(circ, plan.cut))
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[tm] = eng.run(plan.x_p, window, 0, plan.branch_space).amps
+    finally:
+        eng.set_option("tile_major", 2)
+    assert np.array_equal(got[0], got[1]) and np.abs(got[0]).max() > 0
