@@ -84,8 +84,12 @@ def cpu_model() -> str:
     return platform.processor() or "unknown"
 
 
+# prefixes per GPU per step (one run_batched call).  cfg4: 1,024 prefixes x 8 branches; the
+# device rate is flat in the window (115.1k / 116.4k / 116.9k / 117.2k paths/s at 256 / 512 /
+# 1,024 / 2,048, profiles/r02p_*), the public-API call's fixed cost (8 MB of requests up,
+# 16 MB of amplitudes down) is amortised over 4x more paths than at 256 (e2e 104.7k -> 114.2k)
 DEFAULT_WINDOW = {"cfg1": 16, "cfg1v2": 32, "cfg2": 32768, "cfg2v2": 32768, "cfg2h": 2048,
-                  "cfg3": 256, "cfg3v2": 128, "cfg4": 256, "cfg4v2": 128, "cfg5": 1, "cfg5v2": 1, "cfg5f": 1}
+                  "cfg3": 256, "cfg3v2": 128, "cfg4": 1024, "cfg4v2": 512, "cfg5": 1, "cfg5v2": 1, "cfg5f": 1}
 
 
 def describe(name, plan, window, n_req):
