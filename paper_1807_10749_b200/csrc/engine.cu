@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -186,6 +187,17 @@ struct Program {
   std::vector<int> xq[2];
 };
 
+// Pauli frame of a leaf level (pauli_frame below)
+struct PauliFrame {
+  bool ok = false;
+  int nk = 0;
+  int zsel[8][16] = {};           // cross term d of gate j = x0[j][d] * Z^zsel[j][d]
+  double x0[8][16][2] = {};
+  int a[8] = {};                  // behind the level's ops that Z is i^a X^f Z^z
+  uint32_t f[8] = {}, z[8] = {};  // state-bit masks (X part, Z part)
+  int order[8] = {};              // product order, leftmost factor first
+};
+
 struct Ctx {
   int device = -1;
   int precision = GS_C64;
@@ -278,12 +290,19 @@ struct Ctx {
   int proj_fuse = 1;          // option: fuse the other side's last leaf pass with the projected gather (JIT)
   int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
+  int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
   int pf_tail = 0;            // option: the fused pass's last one-qubit-op stage runs per request in its epilogue
                               // (measured: cfg4 -1.3%, cfg4v2 +2%, cfg3v2 equal; off)
   bool proj_fused_active = false;  // the fused projected-leaf pass is compiled for the loaded program
   int64_t pf_rows = 0;        // partial rows written by the current leaf chunk's fused pass
   DevBuf d_proj;              // device copy of ProjProgD for the fused pass
   DevBuf d_pftab, d_pfaoff, d_bmeta;  // fused pass: per-group factor tables, per-bucket-slot request data
+  DevBuf d_pfbflip;                   // Pauli-sibling pass: per-slot park flip | sign mask
+  PauliFrame pauli;                   // Pauli frame of the grouped side's leaf level (ok = the pass is planned)
+  uint32_t pauli_lcol[16] = {};       // park address map L of the Pauli-sibling pass: lcol[j] = L e_j (tile bit j)
+  uint32_t pauli_lit[16] = {};        // L^-T e_j
+  int pauli_conflicts = 0;            // worst bank multiplicity of a warp's park store under L
+  bool pauli_blocked = false;         // the Pauli-sibling kernel did not compile for this program: planned without it
   const int32_t* cur_parent = nullptr;             // device node tables of the current leaf chunk
   const int32_t* cur_gpar = nullptr;               // per leaf group: shared parent of a sibling block, or -1
   bool proj_fast = false;                          // run gates radix 2 with v(d) = d
@@ -749,6 +768,262 @@ static bool projectable(const Ctx& c, int side) {
   return true;
 }
 
+// Pauli frame of a leaf side whose cross terms are x0 * Z^z (the I / Z side of
+// a CZ cut).  A cross term Z inserted before the level's remaining ops O equals
+// the Pauli P = O Z O^+ applied after them when every op maps the running
+// Pauli to a Pauli (H, X^1/2, Y^1/2, CZ: Clifford; T and other diagonals while
+// the Pauli is Z-type on their qubits), so every leaf of a parent is a Pauli
+// image of ONE state, base = O psi (no cross terms):
+//   leaf_d = prod_j x0_j(d_j) * P_j^zsel_j(d_j) base,
+//   (i^a X^f Z^z phi)[x] = i^a (-1)^(z.f) (-1)^(z.x) phi[x ^ f].
+// The conjugations are done numerically on the ops' own matrices (2x2 / 4x4)
+// and matched against the Pauli group, so any gate set is handled: a level
+// that is not Pauli-compatible simply returns ok = false.
+static PauliFrame pauli_frame(const Ctx& c, int side, const std::vector<HostOp>& ops) {
+  using cd = std::complex<double>;
+  PauliFrame pf;
+  const Program& p = c.prog;
+  const int D = (int)p.levels.size() - 1;
+  if (D < 1) return pf;
+  const Level& L = p.levels[D];
+  const int nk = L.k_hi - L.k_lo;
+  if (nk < 1 || nk > 8 || p.q[side] > 31) return pf;
+  pf.nk = nk;
+  const cd iu(0.0, 1.0);
+  const cd ph[4] = {cd(1, 0), iu, cd(-1, 0), -iu};
+  auto pauli_mat = [](int n, int fm, int zm, cd* M) {  // X^fm Z^zm on n qubits, local bit n-1 = first qubit
+    const int dim = 1 << n;
+    for (int i = 0; i < dim * dim; ++i) M[i] = 0.0;
+    for (int y = 0; y < dim; ++y) M[(y ^ fm) * dim + y] = (__builtin_popcount(zm & y) & 1) ? -1.0 : 1.0;
+  };
+  std::vector<std::pair<int, int>> pos;  // (position of the cross op in the list, gate)
+  for (int j = 0; j < nk; ++j) {
+    const int k = L.k_lo + j;
+    if (!p.xdiag[side][k] || p.radix[k] > 16) return pf;
+    for (int d = 0; d < p.radix[k]; ++d) {
+      const double* x = &p.coef[2 * (size_t)p.xtable[p.xtab[side][k] + d]];
+      const cd x0(x[0], x[1]), x1(x[2], x[3]);
+      const double tol = 1e-12 * std::max(1e-300, std::abs(x0));
+      if (std::abs(x0) == 0.0) return pf;
+      if (std::abs(x1 - x0) <= tol) pf.zsel[j][d] = 0;
+      else if (std::abs(x1 + x0) <= tol) pf.zsel[j][d] = 1;
+      else return pf;
+      pf.x0[j][d][0] = x[0], pf.x0[j][d][1] = x[1];
+    }
+    int at = -1, sb = -1;
+    for (size_t i = 0; i < ops.size(); ++i)
+      if (ops[i].cross == k) {
+        if (at >= 0) return pf;
+        at = (int)i, sb = ops[i].s0;
+      }
+    if (at < 0 || sb < 0) return pf;
+    pos.push_back({at, j});
+    // push Z on state bit sb through the ops behind the cross term
+    int a = 0;
+    uint32_t f = 0, z = 1u << sb;
+    for (size_t i = (size_t)at + 1; i < ops.size(); ++i) {
+      const HostOp& op = ops[i];
+      if (op.cross >= 0) continue;  // other cross terms are diagonal in Z ... checked below
+      const bool two = op.kind == K_DIAG2 || op.kind == K_MAT2;
+      const int b1 = op.s0, b0 = two ? op.s1 : -1;  // local bit 1 (high) = s0, local bit 0 = s1
+      if (two && b0 == b1) return pf;
+      const int n = two ? 2 : 1, dim = 1 << n;
+      auto lbit = [&](uint32_t m) {
+        return two ? (int)(((m >> b1) & 1u) << 1 | ((m >> b0) & 1u)) : (int)((m >> b1) & 1u);
+      };
+      const int fm = lbit(f), zm = lbit(z);
+      if (fm == 0 && zm == 0) continue;
+      cd U[16], S[16], R[16];
+      const double* u = &p.coef[2 * (size_t)op.coef];
+      for (int e = 0; e < dim * dim; ++e) U[e] = 0.0;
+      if (op.diag())
+        for (int e = 0; e < dim; ++e) U[e * dim + e] = cd(u[2 * e], u[2 * e + 1]);
+      else
+        for (int e = 0; e < dim * dim; ++e) U[e] = cd(u[2 * e], u[2 * e + 1]);
+      pauli_mat(n, fm, zm, S);
+      for (int r = 0; r < dim; ++r)
+        for (int q2 = 0; q2 < dim; ++q2) {
+          cd acc = 0.0;
+          for (int k2 = 0; k2 < dim; ++k2)
+            for (int l2 = 0; l2 < dim; ++l2) acc += U[r * dim + k2] * S[k2 * dim + l2] * std::conj(U[q2 * dim + l2]);
+          R[r * dim + q2] = acc;
+        }
+      bool found = false;
+      for (int fm2 = 0; fm2 < dim && !found; ++fm2)
+        for (int zm2 = 0; zm2 < dim && !found; ++zm2) {
+          cd C[16];
+          pauli_mat(n, fm2, zm2, C);
+          for (int t = 0; t < 4 && !found; ++t) {
+            double err = 0;
+            for (int e = 0; e < dim * dim; ++e) err = std::max(err, std::abs(R[e] - ph[t] * C[e]));
+            if (err <= 1e-9) {
+              found = true;
+              a = (a + t) & 3;
+              auto put = [&](uint32_t& m, int v) {
+                m &= ~(1u << b1);
+                if (two) m &= ~(1u << b0);
+                if (two) m |= (uint32_t)((v >> 1) & 1) << b1 | (uint32_t)(v & 1) << b0;
+                else m |= (uint32_t)(v & 1) << b1;
+              };
+              put(f, fm2);
+              put(z, zm2);
+            }
+          }
+        }
+      if (!found) return pf;
+    }
+    pf.a[j] = a, pf.f[j] = f, pf.z[j] = z;
+  }
+  // a later cross term must commute with the Z being pushed through it: all are diagonal (checked: xdiag)
+  // but the pushed Pauli may have picked up an X part on that qubit by then -- x0 Z^z X = +-X x0 Z^z,
+  // a sign the frame above does not track.  Reject that (rare) case.
+  for (int j = 0; j < nk; ++j) {
+    const int k = L.k_lo + j;
+    int at = -1;
+    for (size_t i = 0; i < ops.size(); ++i)
+      if (ops[i].cross == k) at = (int)i;
+    for (int j2 = 0; j2 < nk; ++j2) {
+      if (j2 == j) continue;
+      int at2 = -1, sb2 = -1;
+      for (size_t i = 0; i < ops.size(); ++i)
+        if (ops[i].cross == L.k_lo + j2) at2 = (int)i, sb2 = ops[i].s0;
+      if (at2 <= at) continue;
+      // the Z of gate j passes cross term j2 (at position at2): recompute its X part up to there
+      // conservatively: reject when any op between them touches bit sb2 non-diagonally
+      for (int i = at + 1; i < at2; ++i)
+        if (ops[i].cross < 0 && !ops[i].diag() && (ops[i].s0 == sb2 || ops[i].s1 == sb2)) return pf;
+    }
+  }
+  std::sort(pos.begin(), pos.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) { return x.first > y.first; });
+  for (int i = 0; i < nk; ++i) pf.order[i] = pos[i].second;
+  pf.ok = true;
+  return pf;
+}
+
+// GF(2) helpers for the parked-tile address map (K x K bit matrices, rows as masks)
+static uint32_t gf2_apply(const uint32_t* rows, int K, uint32_t v) {
+  uint32_t o = 0;
+  for (int i = 0; i < K; ++i) o |= (uint32_t)(__builtin_popcount(rows[i] & v) & 1) << i;
+  return o;
+}
+static bool gf2_inverse(const uint32_t* rows, int K, uint32_t* inv) {
+  uint32_t a[16], b[16];
+  for (int i = 0; i < K; ++i) a[i] = rows[i], b[i] = 1u << i;
+  for (int col = 0; col < K; ++col) {
+    int piv = -1;
+    for (int r = col; r < K; ++r)
+      if ((a[r] >> col) & 1u) { piv = r; break; }
+    if (piv < 0) return false;
+    std::swap(a[piv], a[col]);
+    std::swap(b[piv], b[col]);
+    for (int r = 0; r < K; ++r)
+      if (r != col && ((a[r] >> col) & 1u)) a[r] ^= a[col], b[r] ^= b[col];
+  }
+  for (int i = 0; i < K; ++i) inv[i] = b[i];
+  return true;
+}
+static int gf2_rank(std::vector<uint32_t> v) {
+  int rank = 0;
+  for (int bit = 0; bit < 32; ++bit) {
+    int piv = -1;
+    for (size_t i = rank; i < v.size(); ++i)
+      if ((v[i] >> bit) & 1u) { piv = (int)i; break; }
+    if (piv < 0) continue;
+    std::swap(v[piv], v[rank]);
+    for (size_t i = 0; i < v.size(); ++i)
+      if ((int)i != rank && ((v[i] >> bit) & 1u)) v[i] ^= v[rank];
+    ++rank;
+  }
+  return rank;
+}
+
+// Address map of the Pauli-sibling pass's parked tile: an invertible GF(2)-linear
+// L on the K tile bits with L f_b = e_b for the flips f_b of the last three cross
+// gates (sibling bit b), so the 8 siblings of a request are one 64-byte run of
+// the parked base tile (sibling pair s, s + 1 = one aligned 16 bytes).  Built as
+// L = S M^-1: M's columns are the independent flips followed by unit vectors
+// (the last stage's lane bits first), S xors three upper address bits into the
+// low three so a warp's park stores spread over the banks.
+static void plan_pauli_layout(Ctx& c) {
+  for (int j = 0; j < 16; ++j) c.pauli_lcol[j] = c.pauli_lit[j] = 1u << j;
+  if (!c.pauli.ok) return;
+  const Program& p = c.prog;
+  const int D = (int)p.levels.size() - 1, side = 1 - c.proj_side;
+  const PassPlan& pp = p.levels[D].passes[side].back();
+  const int K = pp.k, nk = c.pauli.nk;
+  std::vector<int> tpos(p.q[side], -1);
+  for (int j = 0; j < K; ++j) tpos[pp.lbits[j]] = j;
+  auto local = [&](uint32_t m) {
+    uint32_t o = 0;
+    for (int b = 0; b < p.q[side]; ++b)
+      if ((m >> b) & 1u) o |= 1u << tpos[b];
+    return o;
+  };
+  std::vector<uint32_t> cols(K, 0), have;
+  std::vector<char> filled(K, 0);
+  for (int b = 0; b < 3 && b < nk; ++b) {
+    const uint32_t g = local(c.pauli.f[nk - 1 - b]);
+    std::vector<uint32_t> t = have;
+    t.push_back(g);
+    if (g != 0 && gf2_rank(t) == (int)t.size()) cols[b] = g, filled[b] = 1, have = t;
+  }
+  std::vector<int> pref;  // unit vectors: lane bits of the last stage first
+  const PStage& last = c.host_pstages[pp.dev_stage_offset + pp.stages.size() - 1];
+  for (int j = 0; j < 5 && j < K - pp.M; ++j) pref.push_back(last.tb[j]);
+  for (int j = 0; j < K; ++j)
+    if (std::find(pref.begin(), pref.end(), j) == pref.end()) pref.push_back(j);
+  // upper positions (3..K-1) take the preferred bits first, the unfilled low positions what is left
+  std::vector<int> slots;
+  for (int i = 3; i < K; ++i) slots.push_back(i);
+  for (int i = 0; i < 3 && i < K; ++i)
+    if (!filled[i]) slots.push_back(i);
+  size_t si = 0;
+  for (int j : pref) {
+    if (si >= slots.size()) break;
+    std::vector<uint32_t> t = have;
+    t.push_back(1u << j);
+    if (gf2_rank(t) != (int)t.size()) continue;
+    cols[slots[si++]] = 1u << j;
+    have = t;
+  }
+  uint32_t M[16] = {}, Mi[16] = {};
+  for (int i = 0; i < K; ++i)
+    for (int j = 0; j < K; ++j) M[i] |= ((cols[j] >> i) & 1u) << j;
+  if (!gf2_inverse(M, K, Mi)) throw GsError(GS_ERR_STATE, "pauli layout: singular basis");
+  // S: low three address bits ^= address bits sh .. sh + 2; pick sh by the park stores' bank conflicts
+  int best_sh = -1, best_cost = 1 << 30;
+  uint32_t best_rows[16] = {};
+  for (int sh = 3; sh + 3 <= K; ++sh) {
+    uint32_t rows[16];
+    for (int i = 0; i < K; ++i) rows[i] = Mi[i];
+    for (int r = 0; r < 3; ++r) rows[r] ^= Mi[sh + r];
+    int worst = 1;
+    for (int half = 0; half < 2; ++half) {
+      int cnt[16] = {0};
+      for (int l = 0; l < 16; ++l) {
+        uint32_t t = 0;
+        const int lane = l + 16 * half;
+        for (int j = 0; j < 5 && j < K - pp.M; ++j)
+          if ((lane >> j) & 1) t |= 1u << last.tb[j];
+        worst = std::max(worst, ++cnt[gf2_apply(rows, K, t) & 15u]);
+      }
+    }
+    if (worst < best_cost) {
+      best_cost = worst, best_sh = sh;
+      for (int i = 0; i < K; ++i) best_rows[i] = rows[i];
+    }
+  }
+  if (best_sh < 0)
+    for (int i = 0; i < K; ++i) best_rows[i] = Mi[i];
+  uint32_t inv[16] = {};
+  if (!gf2_inverse(best_rows, K, inv)) throw GsError(GS_ERR_STATE, "pauli layout: singular map");
+  for (int j = 0; j < K; ++j) {
+    c.pauli_lcol[j] = gf2_apply(best_rows, K, 1u << j);
+    c.pauli_lit[j] = inv[j];  // row j of L^-1 = column j of L^-T
+  }
+  c.pauli_conflicts = best_cost;
+}
+
 static void schedule_program(Ctx& c) {
   Program& p = c.prog;
   ++c.sched_serial;
@@ -765,6 +1040,7 @@ static void schedule_program(Ctx& c) {
   }
   const int D = (int)p.levels.size() - 1;
   c.proj_side = -1;
+  c.pauli = PauliFrame{};
   if (c.proj_leaf && c.grouped_leaf && !c.fuse_gather && c.kernel_version == 2)
     for (int side = 0; side < 2 && c.proj_side < 0; ++side)
       if (projectable(c, side)) c.proj_side = side;
@@ -809,10 +1085,41 @@ static void schedule_program(Ctx& c) {
         L.passes[side].clear();
         continue;
       }
+      // Pauli-sibling leaf (option pf_pauli): the grouped side of a fused projected leaf whose
+      // cross terms are x0 * Z^z and whose leaf ops keep that Z a Pauli -- one pass without
+      // cross terms or slot bits evolves the base state of each leaf group
+      bool pauli = false;
+      if ((int)l == D && c.pf_pauli && !c.pauli_blocked && c.proj_fuse && c.grouped_leaf && c.proj_side == 1 - side &&
+          c.precision == GS_C64 && c.use_jit && !c.pipeline && c.group_log == 3 && L.k_hi - L.k_lo >= 1 &&
+          L.k_hi - L.k_lo <= 5) {
+        PauliFrame pf = pauli_frame(c, side, work[side][l]);
+        if (pf.ok) {
+          std::vector<HostOp> nc;
+          for (const HostOp& op : work[side][l])
+            if (op.cross < 0) nc.push_back(op);
+          std::vector<PassPlan> ps = schedule_passes(nc, p.q[side], c.kmax(), c.low_bits, true);
+          uint32_t need = 0, have = 0;
+          for (int j = 0; j < pf.nk; ++j) need |= pf.f[j] | pf.z[j];
+          if (ps.size() == 1)
+            for (int b : ps[0].lbits) have |= 1u << b;
+          if (ps.size() == 1 && ps[0].k >= 10 && ps[0].k <= 16 && (need & ~have) == 0) {
+            ps[0].level = (int)l;
+            ps[0].proj_fused = true;
+            ps[0].pf_pauli = true;
+            L.passes[side] = std::move(ps);
+            c.pauli = pf;
+            c.tail_ops[side].clear();
+            c.tail_bits[side].clear();
+            pauli = true;
+          }
+        }
+      }
+      if (!pauli) {
       L.passes[side] = schedule_passes(work[side][l], p.q[side], kcap, c.low_bits, true);
       for (PassPlan& pp : L.passes[side]) pp.level = (int)l;
       if ((int)l == D) extract_tail(c, L, side);
-      if ((int)l == D && c.grouped_leaf) {
+      }
+      if ((int)l == D && c.grouped_leaf && !pauli) {
         L.passes[side].back().grouped_store = true;
         if (side == 1 && c.fuse_gather && c.group_log == 3 && c.precision == GS_C64)
           L.passes[side].back().fused_gather = true;
@@ -887,7 +1194,9 @@ static void schedule_program(Ctx& c) {
         if (pp.grouped_store) pp.K = pp.k + c.group_log;  // the grouped store interleaves 2^G slots
         // complex64 specialised passes use 16-byte HBM accesses (jitgen.inc)
         const bool vec = c.precision == GS_C64 && c.use_jit && c.vec_hbm && (pp.M == 5 || pp.M == 4);
-        pp.stages = schedule_stages(pp, pp.M, vec, pp.grouped_store ? c.group_log : 0,
+        // (the Pauli-sibling pass parks its tile in shared memory: like a grouped store, any last-stage
+        // register set is fine)
+        pp.stages = schedule_stages(pp, pp.M, vec, pp.grouped_store ? c.group_log : (pp.pf_pauli ? 3 : 0),
                                     pp.grouped_store && c.slot_store16 && !c.pipeline);
         pp.dev_stage_offset = (int64_t)c.host_pstages.size();
         pp.goff_offset = (int64_t)c.host_gofftab.size();
@@ -1016,6 +1325,7 @@ static void schedule_program(Ctx& c) {
       }
     }
   }
+  plan_pauli_layout(c);
   // packed-digit lookup per level (fan-outs up to 2^16)
   for (size_t l = 1; l < p.levels.size(); ++l) {
     Level& L = p.levels[l];
@@ -1084,8 +1394,10 @@ static void jit_program(Ctx& c) {
       size_t smem = 0;
       if (pp.proj_fused) {
         const Level& LD = c.prog.levels[pp.level];
-        kernels[t] = jitgen::proj_fused_kernel(c, pp, 0, smem, c.pf_u, LD.k_hi - LD.k_lo,
-                                               min_blocks > 0 ? c.pf_min_blocks : 0);
+        kernels[t] = pp.pf_pauli ? jitgen::proj_pauli_kernel(c, pp, 0, smem, LD.k_hi - LD.k_lo,
+                                                             min_blocks > 0 ? c.pf_min_blocks : 0)
+                                 : jitgen::proj_fused_kernel(c, pp, 0, smem, c.pf_u, LD.k_hi - LD.k_lo,
+                                                             min_blocks > 0 ? c.pf_min_blocks : 0);
       } else {
         kernels[t] = pp.pipelined ? jitgen::pass_kernel_pipe(c, pp, 0, smem)
                                   : jitgen::pass_kernel(c, pp, 0, smem, pp.fused_gather,
@@ -1249,6 +1561,13 @@ static void upload_program(Ctx& c) {
     upload(c, c.d_coef, c.prog.coef);
   }
   jit_program(c);
+  if (c.pauli.ok && !c.proj_fused_active) {
+    // the Pauli-sibling pass exists only as a specialised kernel: without it, plan the grouped-store leaf
+    c.pauli_blocked = true;
+    schedule_program(c);
+    upload_program(c);
+    return;
+  }
   {  // projected leaf side
     ProjProgD pj;
     std::memset(&pj, 0, sizeof pj);
@@ -1323,6 +1642,31 @@ static void upload_program(Ctx& c) {
     CK(cudaMemcpyToSymbol(g_proj, &pj, sizeof pj));
     c.d_proj.ensure(sizeof pj);
     CK(cudaMemcpy(c.d_proj.p, &pj, sizeof pj, cudaMemcpyHostToDevice));
+  }
+  if (c.pauli.ok && c.proj_side >= 0) {  // Pauli-sibling pass: the frame in tile-bit / park-address coordinates
+    PauliProgD pd;
+    std::memset(&pd, 0, sizeof pd);
+    const Program& p = c.prog;
+    const int side = 1 - c.proj_side;
+    const PassPlan& pp = p.levels.back().passes[side].back();
+    std::vector<int> tpos(p.q[side], -1);
+    for (int j = 0; j < pp.k; ++j) tpos[pp.lbits[j]] = j;
+    pd.nk = c.pauli.nk;
+    for (int j = 0; j < pd.nk; ++j) {
+      pd.order[j] = c.pauli.order[j];
+      pd.a[j] = c.pauli.a[j];
+      for (int d = 0; d < 16; ++d) {
+        pd.zsel[j][d] = c.pauli.zsel[j][d];
+        pd.x0[j][d][0] = c.pauli.x0[j][d][0];
+        pd.x0[j][d][1] = c.pauli.x0[j][d][1];
+      }
+      for (int b = 0; b < p.q[side]; ++b) {
+        if ((c.pauli.f[j] >> b) & 1u) pd.f[j] |= 1u << tpos[b], pd.lf[j] ^= c.pauli_lcol[tpos[b]];
+        if ((c.pauli.z[j] >> b) & 1u) pd.z[j] |= 1u << tpos[b], pd.lz[j] ^= c.pauli_lit[tpos[b]];
+      }
+    }
+    for (int j = 0; j < 16; ++j) pd.lcol[j] = c.pauli_lcol[j];
+    CK(cudaMemcpyToSymbol(g_pauli, &pd, sizeof pd));
   }
 }
 
@@ -1491,7 +1835,8 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
   for (int j = 0; j < (int)pp.gbits.size(); ++j) a.gbits[j] = pp.gbits[j];
   const int threads = 1 << (a.K - pp.M);
   const size_t smem = ((size_t)1 << a.K) * c.esize();
-  const int64_t groups = (n_states + (1LL << slots) - 1) >> slots;
+  // (a Pauli-sibling pass evolves one base state per 8-leaf group)
+  const int64_t groups = pp.pf_pauli ? (n_states + 7) >> 3 : (n_states + (1LL << slots) - 1) >> slots;
   const int64_t blocks = groups << a.tiles_log;
   if (blocks > INT32_MAX) throw GsError(GS_ERR_ARG, "grid too large");
   c.st.n_pass_launches++;
@@ -1538,11 +1883,20 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
       c.d_pfaoff.ensure((size_t)ng * 8 * sizeof(long long));
       c.d_partial.ensure(std::max<size_t>((size_t)ng * (size_t)c.n_req * sizeof(double2), 16));
       const void* P = (ps == 0 ? c.lvl_a : c.lvl_b)[D - 1].p;
-      pf_table_kernel<<<(unsigned)ng, 256, 0, c.stream>>>(reinterpret_cast<const unsigned long long*>(digit),
-                                                        c.cur_parent, c.cur_weights, n_states,
-                                                        1LL << c.prog.q[ps],
-                                                        reinterpret_cast<float2*>(c.d_pftab.p),
-                                                        reinterpret_cast<long long*>(c.d_pfaoff.p));
+      if (pp.pf_pauli) {
+        c.d_pfbflip.ensure((size_t)ng * 8 * sizeof(unsigned));
+        pf_table_pauli_kernel<<<(unsigned)ng, 256, 0, c.stream>>>(
+            reinterpret_cast<const unsigned long long*>(digit), c.cur_parent, c.cur_weights, n_states,
+            1LL << c.prog.q[ps], reinterpret_cast<float2*>(c.d_pftab.p),
+            reinterpret_cast<long long*>(c.d_pfaoff.p), reinterpret_cast<unsigned*>(c.d_pfbflip.p));
+        j.pf_bflip = reinterpret_cast<const unsigned*>(c.d_pfbflip.p);
+      } else {
+        pf_table_kernel<<<(unsigned)ng, 256, 0, c.stream>>>(reinterpret_cast<const unsigned long long*>(digit),
+                                                          c.cur_parent, c.cur_weights, n_states,
+                                                          1LL << c.prog.q[ps],
+                                                          reinterpret_cast<float2*>(c.d_pftab.p),
+                                                          reinterpret_cast<long long*>(c.d_pfaoff.p));
+      }
       launch_check("pf_table_kernel", ng, 256, 0);
       c.st.n_launches++;
       j.bstart = reinterpret_cast<const int32_t*>(c.d_bstart.p);
@@ -2154,7 +2508,7 @@ static void build_buckets(Ctx& c) {
     CK(cudaMemsetAsync(reinterpret_cast<int2*>(c.d_bmeta.p) + n, 0, 64 * sizeof(int2), c.stream));
     pf_meta_kernel<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<const int32_t*>(c.d_bia.p),
                                                  reinterpret_cast<const int32_t*>(c.d_btl.p), n,
-                                                 reinterpret_cast<int2*>(c.d_bmeta.p));
+                                                 reinterpret_cast<int2*>(c.d_bmeta.p), pp.pf_pauli ? 1 : 0);
   }
   CK(cudaGetLastError());
   c.bucket_valid = true;
@@ -2361,6 +2715,10 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "pf_u must be in [1, 8]");
       c.pf_u = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_pauli") {
+      c.pf_pauli = value ? 1 : 0;
+      c.pauli_blocked = false;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_tail") {
       c.pf_tail = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -2462,6 +2820,7 @@ int gs_load_program(gs_ctx* ctx, int32_t qa, int32_t qb, int32_t n_ops, const in
       throw GsError(GS_ERR_ARG, "null cross array");
     if (!c.host_only) CK(cudaSetDevice(c.device));
     c.have_prog = false;
+    c.pauli_blocked = false;
     gs::build_program(c, qa, qb, n_ops, op_kind, op_blk, op_q0, op_q1, op_cycle, op_coef, n_cross,
                       cross_rank, cross_cycle, cross_qa, cross_qb, term_kind_a, term_coef_a,
                       term_kind_b, term_coef_b, n_coef, coef);
@@ -2522,7 +2881,16 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
     }
     js += "], \"tail\": [" + std::to_string(c.tail_ops[0].size()) + ", " + std::to_string(c.tail_ops[1].size()) +
           "], \"proj_side\": " + std::to_string(c.proj_side) + ", \"proj_fused\": " +
-          std::to_string(c.proj_fused_active ? 1 : 0) + ", \"opts\": {\"pf_tail\": " + std::to_string(c.pf_tail) +
+          std::to_string(c.proj_fused_active ? 1 : 0) + ", \"pauli\": " + [&]() {
+            if (!c.pauli.ok) return std::string("null");
+            std::string t = "{\"conflicts\": " + std::to_string(c.pauli_conflicts) + ", \"gates\": [";
+            for (int j = 0; j < c.pauli.nk; ++j)
+              t += (j ? ", " : "") + std::string("{\"a\": ") + std::to_string(c.pauli.a[j]) + ", \"f\": " +
+                   std::to_string(c.pauli.f[j]) + ", \"z\": " + std::to_string(c.pauli.z[j]) + "}";
+            t += "], \"lcol\": [";
+            for (int j = 0; j < 16; ++j) t += (j ? ", " : "") + std::to_string(c.pauli_lcol[j]);
+            return t + "]}";
+          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
           ", \"tile_major\": " + std::to_string(c.tile_major) + ", \"pf_min_blocks\": " +
           std::to_string(c.pf_min_blocks) + ", \"pipeline\": " + std::to_string(c.pipeline) + ", \"sink_ops\": " +
           std::to_string(c.sink_ops) + ", \"reg_bits\": " + std::to_string(c.reg_bits) + "}, \"proj_swaps\": " +

@@ -48,6 +48,7 @@ struct JArgs {
   const void* pf_tab;         // float2 [group][8 << nk]: projected factor per sibling and request cross bits
   const long long* pf_aoff;   // [group][8]: parent amplitude offset per sibling
   const void* pf_meta;        // int2 per bucket slot: (tile-local index | cross bits << 16, parent base index)
+  const unsigned* pf_bflip;   // Pauli-sibling pass: [group][8] park-address flip | sign-parity mask << 16 per sibling
 };
 
 struct JitModule;

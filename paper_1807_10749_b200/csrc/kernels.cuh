@@ -608,6 +608,25 @@ struct ProjProgD {
 };
 __constant__ ProjProgD g_proj;
 
+// Pauli frame of the grouped side's leaf level (engine.cu pauli_frame): cross
+// term d of gate j is x0[j][d] * Z^zsel[j][d] on the gate's qubit, and behind
+// the level's other ops that Z is the Pauli i^a[j] X^f[j] Z^z[j].  Masks are in
+// tile-bit coordinates of the Pauli-sibling pass; lf = L f and lz = L^-T z are
+// their images under the parked tile's address map L (lcol[j] = L e_j), so a
+// request at park address A = L t finds sibling s at A ^ lf_s with sign
+// (-1)^popc(A & lz_s).
+struct PauliProgD {
+  int nk;
+  int order[8];          // product order, leftmost factor first
+  int zsel[8][16];
+  double x0[8][16][2];
+  int a[8];
+  unsigned f[8], z[8];
+  unsigned lf[8], lz[8];
+  unsigned lcol[16];
+};
+__constant__ PauliProgD g_pauli;
+
 // Per-leaf factor and source index of the projected side: leaf digits dg,
 // block-local index x -> coefficient prod_k a_k(d_k) U_k[x_k, v_k(d_k)] and the
 // parent index y = x with every cross qubit set to v_k(d_k).  Tables from
@@ -927,9 +946,16 @@ static __global__ void bucket_fill_kernel(const int32_t* ib, const int32_t* ia, 
 // bucket slot, the projected-side index with its leaf-level cross bits cleared
 // and the parent layout's bit swaps applied (abase), and the tile-local index
 // of the grouped side packed with the request's cross bits (tl | xc << 16).
-static __global__ void pf_meta_kernel(const int32_t* bia, const int32_t* btl, long long n, int2* meta) {
+static __global__ void pf_meta_kernel(const int32_t* bia, const int32_t* btl, long long n, int2* meta, int pauli) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  unsigned tl = (unsigned)btl[i];
+  if (pauli) {  // Pauli-sibling pass: the request's address in the parked tile
+    unsigned t = 0;
+    for (int j = 0; j < 16; ++j)
+      if ((tl >> j) & 1u) t ^= g_pauli.lcol[j];
+    tl = t;
+  }
   long long x = bia[i];
   int xc = 0;
   for (int k = 0; k < g_proj.n; ++k) {
@@ -940,7 +966,7 @@ static __global__ void pf_meta_kernel(const int32_t* bia, const int32_t* btl, lo
     const int a = g_proj.sa[w], b = g_proj.sb[w];
     if (((x >> a) & 1) != ((x >> b) & 1)) x ^= (1LL << a) | (1LL << b);
   }
-  meta[i] = make_int2(btl[i] | (xc << 16), (int)x);
+  meta[i] = make_int2((int)tl | (xc << 16), (int)x);
 }
 
 // Fused projected-leaf pass, leaf side: per leaf group g (8 sibling slots) and
@@ -977,6 +1003,69 @@ static __global__ void pf_table_kernel(const unsigned long long* digits, const i
   }
   tab[(g << (3 + nk)) + t] = c;
   if (xc == 0) aoff[(g << 3) + s] = off;
+}
+
+// Pauli-sibling form of the table: the projected factor above times the grouped
+// side's sibling scalar prod_j x0_j(d_j) * i^a (-1)^(z.f) of the slot's Pauli
+// P = prod_j P_j^zsel_j(d_j) (product in g_pauli.order), and per slot the park
+// address flip and sign-parity mask of that Pauli (bflip = lf | lz << 16).
+static __global__ void pf_table_pauli_kernel(const unsigned long long* digits, const int32_t* parent,
+                                             const double* weights, long long n_states, long long p_elems,
+                                             float2* tab, long long* aoff, unsigned* bflip) {
+  const int nk = g_proj.n, t = threadIdx.x;
+  if (t >= (8 << nk)) return;
+  const long long g = blockIdx.x;
+  const int s = t & 7, xc = t >> 3;
+  const long long slot = (g << 3) | s;
+  float2 c = make_float2(0.f, 0.f);
+  long long off = 0;
+  unsigned lf = 0, lz = 0;
+  if (slot < n_states) {
+    const unsigned long long dg = digits[slot];
+    double pr = weights[slot], pi = 0.0;
+    off = (long long)parent[slot] * p_elems;
+    for (int k = 0; k < nk; ++k) {
+      const int d = (int)((dg >> (4 * k)) & 15ull);
+      const int vb = g_proj.v[k][d], xb = (xc >> k) & 1;
+      const double* u = g_proj.u[k] + 2 * (2 * xb + vb);
+      const double fr = g_proj.a[k][d][0] * u[0] - g_proj.a[k][d][1] * u[1];
+      const double fi = g_proj.a[k][d][0] * u[1] + g_proj.a[k][d][1] * u[0];
+      const double tr = pr * fr - pi * fi;
+      pi = pr * fi + pi * fr;
+      pr = tr;
+      off |= (long long)vb << g_proj.abit[k];
+    }
+    int a = 0;
+    unsigned f = 0, z = 0;
+    for (int i = 0; i < g_pauli.nk; ++i) {
+      const int j = g_pauli.order[i];
+      const int d = (int)((dg >> (4 * j)) & 15ull);
+      const double xr = g_pauli.x0[j][d][0], xi = g_pauli.x0[j][d][1];
+      const double tr = pr * xr - pi * xi;
+      pi = pr * xi + pi * xr;
+      pr = tr;
+      if (g_pauli.zsel[j][d]) {  // (i^a X^f Z^z)(i^b X^g Z^h) = i^(a+b) (-1)^(z.g) X^(f^g) Z^(z^h)
+        a += g_pauli.a[j] + 2 * (__popc(z & g_pauli.f[j]) & 1);
+        f ^= g_pauli.f[j];
+        z ^= g_pauli.z[j];
+        lf ^= g_pauli.lf[j];
+        lz ^= g_pauli.lz[j];
+      }
+    }
+    a += 2 * (__popc(z & f) & 1);  // (P phi)[x] = i^a (-1)^(z.f) (-1)^(z.x) phi[x ^ f]
+    switch (a & 3) {
+      case 1: { const double tr = -pi; pi = pr; pr = tr; } break;
+      case 2: pr = -pr, pi = -pi; break;
+      case 3: { const double tr = pi; pi = -pr; pr = tr; } break;
+      default: break;
+    }
+    c = make_float2((float)pr, (float)pi);
+  }
+  tab[(g << (3 + nk)) + t] = c;
+  if (xc == 0) {
+    aoff[(g << 3) + s] = off;
+    bflip[(g << 3) + s] = lf | (lz << 16);
+  }
 }
 
 }  // namespace gs

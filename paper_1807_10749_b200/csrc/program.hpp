@@ -64,6 +64,9 @@ struct PassPlan {
   bool fused_gather = false;    // leaf level, last B pass: gather instead of a B store (JIT)
   bool proj_fused = false;      // leaf level, last pass of the grouped side: fused with the projected-side
                                 // gather (JIT; no leaf state of either side reaches HBM)
+  bool pf_pauli = false;        // proj_fused, Pauli-sibling form: the pass evolves ONE base state per leaf group
+                                // (no cross terms, no slot bits); the siblings are Pauli images of it, read from
+                                // the parked tile at flipped positions with signs
   bool pipelined = false;       // JIT: persistent kernel prefetching the next tile (option pipeline)
   int level = -1;               // path-tree level of the pass
   std::vector<int> store_perm;  // non-empty: state bit b is stored at address bit store_perm[b] (JIT only)

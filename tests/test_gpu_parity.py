@@ -616,14 +616,18 @@ def test_fused_projected_leaf_pass(ps, name):
     circ, plan, req, pre = configs.build(name, n_req=20000)
     eng = _engine("c64")
     got = {}
-    DEFAULTS = {"proj_fuse": 1, "pf_tail": 0, "pf_min_blocks": 3, "tile_major": 2}
+    DEFAULTS = {"proj_fuse": 1, "pf_tail": 0, "pf_min_blocks": 3, "tile_major": 2, "pf_pauli": 1}
     try:
-        for key, opts in (("sep", {"proj_fuse": 0}), ("fused", {}), ("tail", {"pf_tail": 1}),
+        # "fused" is the default: the Pauli-sibling form (one base state per leaf group, siblings read
+        # as Pauli images); "slots" is the 8-slot form it replaces
+        for key, opts in (("sep", {"proj_fuse": 0}), ("fused", {}), ("slots", {"pf_pauli": 0}),
+                          ("tail", {"pf_tail": 1, "pf_pauli": 0}),
                           ("mb0", {"pf_min_blocks": 0}), ("tilemajor", {"tile_major": 1})):
             for k, v in opts.items():
                 eng.set_option(k, v)
             eng.load_program(lowered(circ, plan.cut))
             assert eng.describe()["proj_fused"] == (0 if key == "sep" else 1)
+            assert (eng.describe()["pauli"] is not None) == (key in ("fused", "mb0", "tilemajor"))
             eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
             got[key] = (eng.run(plan.x_p, pre[:9], 0, plan.branch_space).amps,
                         eng.run(plan.x_p, pre[:5], 1, plan.branch_space - 1).amps,
@@ -633,7 +637,7 @@ def test_fused_projected_leaf_pass(ps, name):
     finally:
         for k, v in DEFAULTS.items():
             eng.set_option(k, v)
-    for key in ("fused", "tail", "mb0", "tilemajor"):
+    for key in ("fused", "slots", "tail", "mb0", "tilemajor"):
         for a, b in zip(got["sep"], got[key]):
             assert np.abs(a).max() > 0
             assert rel_l2(b, a) <= 2e-6, key
