@@ -291,6 +291,7 @@ struct Ctx {
   int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
+  int pf_pipe = 1;            // option: software-pipelined epilogue of the Pauli-sibling pass
   int pf_tail = 0;            // option: the fused pass's last one-qubit-op stage runs per request in its epilogue
                               // (measured: cfg4 -1.3%, cfg4v2 +2%, cfg3v2 equal; off)
   bool proj_fused_active = false;  // the fused projected-leaf pass is compiled for the loaded program
@@ -1394,8 +1395,10 @@ static void jit_program(Ctx& c) {
       size_t smem = 0;
       if (pp.proj_fused) {
         const Level& LD = c.prog.levels[pp.level];
+        // (the Pauli-sibling pass: 2 CTAs/SM, 128 registers -- at the 3-CTA bound its pipelined
+        // epilogue spills, measured 6% slower)
         kernels[t] = pp.pf_pauli ? jitgen::proj_pauli_kernel(c, pp, 0, smem, LD.k_hi - LD.k_lo,
-                                                             min_blocks > 0 ? c.pf_min_blocks : 0)
+                                                             min_blocks > 0 ? std::min(c.pf_min_blocks, 2) : 0)
                                  : jitgen::proj_fused_kernel(c, pp, 0, smem, c.pf_u, LD.k_hi - LD.k_lo,
                                                              min_blocks > 0 ? c.pf_min_blocks : 0);
       } else {
@@ -2715,6 +2718,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "pf_u must be in [1, 8]");
       c.pf_u = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_pipe") {
+      c.pf_pipe = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_pauli") {
       c.pf_pauli = value ? 1 : 0;
       c.pauli_blocked = false;
@@ -2890,7 +2896,7 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
             t += "], \"lcol\": [";
             for (int j = 0; j < 16; ++j) t += (j ? ", " : "") + std::to_string(c.pauli_lcol[j]);
             return t + "]}";
-          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
+          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_pipe\": " + std::to_string(c.pf_pipe) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
           ", \"tile_major\": " + std::to_string(c.tile_major) + ", \"pf_min_blocks\": " +
           std::to_string(c.pf_min_blocks) + ", \"pipeline\": " + std::to_string(c.pipeline) + ", \"sink_ops\": " +
           std::to_string(c.sink_ops) + ", \"reg_bits\": " + std::to_string(c.reg_bits) + "}, \"proj_swaps\": " +
