@@ -196,6 +196,7 @@ struct PauliFrame {
   int a[8] = {};                  // behind the level's ops that Z is i^a X^f Z^z
   uint32_t f[8] = {}, z[8] = {};  // state-bit masks (X part, Z part)
   int order[8] = {};              // product order, leftmost factor first
+  bool projector = false;         // some term is a projector a (I + (-1)^v Z) / 2 (zsel = 2 + v)
 };
 
 struct Ctx {
@@ -291,6 +292,8 @@ struct Ctx {
   int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
+  int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
+                              // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
   int pf_pipe = 1;            // option: software-pipelined epilogue of the Pauli-sibling pass
   int pf_tail = 0;            // option: the fused pass's last one-qubit-op stage runs per request in its epilogue
                               // (measured: cfg4 -1.3%, cfg4v2 +2%, cfg3v2 equal; off)
@@ -804,8 +807,16 @@ static PauliFrame pauli_frame(const Ctx& c, int side, const std::vector<HostOp>&
     for (int d = 0; d < p.radix[k]; ++d) {
       const double* x = &p.coef[2 * (size_t)p.xtable[p.xtab[side][k] + d]];
       const cd x0(x[0], x[1]), x1(x[2], x[3]);
-      const double tol = 1e-12 * std::max(1e-300, std::abs(x0));
-      if (std::abs(x0) == 0.0) return pf;
+      const double tol = 1e-12 * std::max(1e-300, std::max(std::abs(x0), std::abs(x1)));
+      if (std::abs(x0) <= tol && std::abs(x1) <= tol) return pf;
+      if (std::abs(x0) <= tol || std::abs(x1) <= tol) {
+        // projector term a * (I + (-1)^v Z) / 2 (the P0 / P1 side of a CZ cut): zsel = 2 + v, x0 = a
+        const int v = std::abs(x0) <= tol ? 1 : 0;
+        pf.zsel[j][d] = 2 + v;
+        pf.x0[j][d][0] = x[2 * v], pf.x0[j][d][1] = x[2 * v + 1];
+        pf.projector = true;
+        continue;
+      }
       if (std::abs(x1 - x0) <= tol) pf.zsel[j][d] = 0;
       else if (std::abs(x1 + x0) <= tol) pf.zsel[j][d] = 1;
       else return pf;
@@ -1094,7 +1105,7 @@ static void schedule_program(Ctx& c) {
           c.precision == GS_C64 && c.use_jit && !c.pipeline && c.group_log == 3 && L.k_hi - L.k_lo >= 1 &&
           L.k_hi - L.k_lo <= 5) {
         PauliFrame pf = pauli_frame(c, side, work[side][l]);
-        if (pf.ok) {
+        if (pf.ok && !pf.projector) {
           std::vector<HostOp> nc;
           for (const HostOp& op : work[side][l])
             if (op.cross < 0) nc.push_back(op);
@@ -2718,6 +2729,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "pf_u must be in [1, 8]");
       c.pf_u = (int)value;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "xchg16") {
+      c.xchg16 = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_pipe") {
       c.pf_pipe = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -2887,7 +2901,10 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
     }
     js += "], \"tail\": [" + std::to_string(c.tail_ops[0].size()) + ", " + std::to_string(c.tail_ops[1].size()) +
           "], \"proj_side\": " + std::to_string(c.proj_side) + ", \"proj_fused\": " +
-          std::to_string(c.proj_fused_active ? 1 : 0) + ", \"pauli\": " + [&]() {
+          std::to_string(c.proj_fused_active ? 1 : 0) + ", \"pauli_sides\": [" +
+          std::to_string(gs::pauli_frame(c, 0, c.prog.levels.back().ops[0]).ok ? 1 : 0) + ", " +
+          std::to_string(c.prog.q[1] > 0 && gs::pauli_frame(c, 1, c.prog.levels.back().ops[1]).ok ? 1 : 0) +
+          "], \"pauli\": " + [&]() {
             if (!c.pauli.ok) return std::string("null");
             std::string t = "{\"conflicts\": " + std::to_string(c.pauli_conflicts) + ", \"gates\": [";
             for (int j = 0; j < c.pauli.nk; ++j)
@@ -2896,7 +2913,7 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
             t += "], \"lcol\": [";
             for (int j = 0; j < 16; ++j) t += (j ? ", " : "") + std::to_string(c.pauli_lcol[j]);
             return t + "]}";
-          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_pipe\": " + std::to_string(c.pf_pipe) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
+          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_pipe\": " + std::to_string(c.pf_pipe) + ", \"xchg16\": " + std::to_string(c.xchg16) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
           ", \"tile_major\": " + std::to_string(c.tile_major) + ", \"pf_min_blocks\": " +
           std::to_string(c.pf_min_blocks) + ", \"pipeline\": " + std::to_string(c.pipeline) + ", \"sink_ops\": " +
           std::to_string(c.sink_ops) + ", \"reg_bits\": " + std::to_string(c.reg_bits) + "}, \"proj_swaps\": " +
