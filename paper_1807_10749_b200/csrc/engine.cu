@@ -294,6 +294,8 @@ struct Ctx {
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
   int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
                               // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
+  int pf_groups = 2;          // option: leaf groups a Pauli-sibling CTA serves back to back into one partial row
+                              // (cfg4: 1: 168.1k, 2: 171.9k, 4: 171.1k, 8: 169.9k paths/s)
   int pf_pipe = 1;            // option: software-pipelined epilogue of the Pauli-sibling pass
   int pf_tail = 0;            // option: the fused pass's last one-qubit-op stage runs per request in its epilogue
                               // (measured: cfg4 -1.3%, cfg4v2 +2%, cfg3v2 equal; off)
@@ -1891,11 +1893,13 @@ static void launch_pass2(Ctx& c, int side, const PassPlan& pp, const void* src, 
       const int D = (int)c.prog.levels.size() - 1;
       const int nk = c.prog.levels[D].k_hi - c.prog.levels[D].k_lo;
       const int64_t ng = (n_states + 7) >> 3;
-      c.pf_rows = ng;
+      const int64_t gpc = pp.pf_pauli ? std::max(1, c.pf_groups) : 1;  // groups per CTA = per partial row
+      c.pf_rows = (ng + gpc - 1) / gpc;
+      if (pp.pf_pauli) grid = c.pf_rows << a.tiles_log;
       if (c.n_req <= 0) return;
       c.d_pftab.ensure((size_t)ng * ((size_t)8 << nk) * sizeof(float2));
       c.d_pfaoff.ensure((size_t)ng * 8 * sizeof(long long));
-      c.d_partial.ensure(std::max<size_t>((size_t)ng * (size_t)c.n_req * sizeof(double2), 16));
+      c.d_partial.ensure(std::max<size_t>((size_t)c.pf_rows * (size_t)c.n_req * sizeof(double2), 16));
       const void* P = (ps == 0 ? c.lvl_a : c.lvl_b)[D - 1].p;
       if (pp.pf_pauli) {
         c.d_pfbflip.ensure((size_t)ng * 8 * sizeof(unsigned));
@@ -2732,6 +2736,10 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "xchg16") {
       c.xchg16 = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_groups") {
+      if (value < 1 || value > 64) throw GsError(GS_ERR_ARG, "pf_groups must be in [1, 64]");
+      c.pf_groups = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_pipe") {
       c.pf_pipe = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -2913,7 +2921,7 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
             t += "], \"lcol\": [";
             for (int j = 0; j < 16; ++j) t += (j ? ", " : "") + std::to_string(c.pauli_lcol[j]);
             return t + "]}";
-          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_pipe\": " + std::to_string(c.pf_pipe) + ", \"xchg16\": " + std::to_string(c.xchg16) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
+          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_pipe\": " + std::to_string(c.pf_pipe) + ", \"pf_groups\": " + std::to_string(c.pf_groups) + ", \"xchg16\": " + std::to_string(c.xchg16) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
           ", \"tile_major\": " + std::to_string(c.tile_major) + ", \"pf_min_blocks\": " +
           std::to_string(c.pf_min_blocks) + ", \"pipeline\": " + std::to_string(c.pipeline) + ", \"sink_ops\": " +
           std::to_string(c.sink_ops) + ", \"reg_bits\": " + std::to_string(c.reg_bits) + "}, \"proj_swaps\": " +
