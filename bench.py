@@ -382,9 +382,9 @@ def main():
             w = windows[s]
             if world > 1:
                 union = np.concatenate([all_windows[r][s] for r in range(world)])
-                run_batched_sharded(circ, plan, req, prefixes=union, dst=None, device=local)
+                run_batched_sharded(circ, plan, req, prefixes=union, dst=None, device=local, dtype=args.dtype)
             else:
-                run_batched(circ, plan, req, prefixes=w, device=local)
+                run_batched(circ, plan, req, prefixes=w, device=local, dtype=args.dtype)
             return w.size * plan.branch_space * world
 
         for s in range(min(args.warmup, 2)):  # untimed warm-up of the public-API path

@@ -294,6 +294,10 @@ struct Ctx {
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
   int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
                               // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
+  int pf_streams = 1;         // option: Pauli-sibling pass requests in two bank-half streams per tile, sorted by
+                              // factor-table row (conflict-free park reads, broadcast factor reads)
+  int l2_ahead = 148;         // option: pass CTAs prefetch into L2 the stage-0 tile of the CTA this many launches later
+                              // (0 off; cfg4: 0: 171.2k, 74: 178.5k, 148: 177.9k, 222: 178.3k, 296: 175.2k, 444: 169.0k)
   int pf_groups = 2;          // option: leaf groups a Pauli-sibling CTA serves back to back into one partial row
                               // (cfg4: 1: 168.1k, 2: 171.9k, 4: 171.1k, 8: 169.9k paths/s)
   int pf_pipe = 1;            // option: software-pipelined epilogue of the Pauli-sibling pass
@@ -305,6 +309,14 @@ struct Ctx {
   DevBuf d_pftab, d_pfaoff, d_bmeta;  // fused pass: per-group factor tables, per-bucket-slot request data
   DevBuf d_pfbflip;                   // Pauli-sibling pass: per-slot park flip | sign mask
   PauliFrame pauli;                   // Pauli frame of the grouped side's leaf level (ok = the pass is planned)
+  // Pauli-sibling leaves of the path-major gathers (half-states too large for the grouped layout):
+  // side psib_side's leaf passes evolve one base state per parent, without cross terms; the
+  // gather reads every leaf of that side as a Pauli image of its parent's base state
+  PauliFrame psib;
+  int psib_side = -1;
+  const void* cur_sib = nullptr;        // device SibD per leaf of the current leaf chunk
+  const int32_t* cur_upar = nullptr;    // device: distinct parents of the current leaf chunk
+  int64_t cur_npar = 0;
   uint32_t pauli_lcol[16] = {};       // park address map L of the Pauli-sibling pass: lcol[j] = L e_j (tile bit j)
   uint32_t pauli_lit[16] = {};        // L^-T e_j
   int pauli_conflicts = 0;            // worst bank multiplicity of a warp's park store under L
@@ -1055,6 +1067,8 @@ static void schedule_program(Ctx& c) {
   const int D = (int)p.levels.size() - 1;
   c.proj_side = -1;
   c.pauli = PauliFrame{};
+  c.psib = PauliFrame{};
+  c.psib_side = -1;
   if (c.proj_leaf && c.grouped_leaf && !c.fuse_gather && c.kernel_version == 2)
     for (int side = 0; side < 2 && c.proj_side < 0; ++side)
       if (projectable(c, side)) c.proj_side = side;
@@ -1126,6 +1140,21 @@ static void schedule_program(Ctx& c) {
             c.tail_bits[side].clear();
             pauli = true;
           }
+        }
+      }
+      if (!pauli && (int)l == D && D >= 1 && c.pf_pauli && side == 1 && c.kernel_version == 2 && !c.grouped_leaf &&
+          plain_gather(c) && p.q[side] >= 5 && p.q[side] <= 31 && L.k_hi - L.k_lo >= 1 && L.k_hi - L.k_lo <= 8) {
+        PauliFrame pf = pauli_frame(c, side, work[side][l]);
+        if (pf.ok && !pf.projector) {
+          std::vector<HostOp> nc;
+          for (const HostOp& op : work[side][l])
+            if (op.cross < 0) nc.push_back(op);
+          L.passes[side] = schedule_passes(nc, p.q[side], kcap, c.low_bits, true);
+          for (PassPlan& pp : L.passes[side]) pp.level = (int)l;
+          extract_tail(c, L, side);
+          c.psib = pf;
+          c.psib_side = side;
+          pauli = true;
         }
       }
       if (!pauli) {
@@ -1981,10 +2010,11 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
       continue;
     }
     double b = 0;
+    const double ns = (l == D && side == c.psib_side) ? (double)c.cur_npar : (double)n;  // states this side writes
     for (size_t i = 0; i < L.passes[side].size(); ++i) {
       const PassPlan& pp = L.passes[side][i];
-      const double rd = i == 0 ? (root ? 0.0 : (double)n_parents * sb) : (double)n * sb;
-      const double wr = (pp.proj_fused && c.proj_fused_active) ? 0.0 : (double)n * sb;
+      const double rd = i == 0 ? (root ? 0.0 : (double)n_parents * sb) : ns * sb;
+      const double wr = (pp.proj_fused && c.proj_fused_active) ? 0.0 : ns * sb;
       b += rd + wr;
       if (l == D) c.st.n_leaf_launches++;
     }
@@ -1997,7 +2027,14 @@ static void run_level_passes(Ctx& c, int l, int64_t n, const void* src_a, const 
     for (const PassPlan& pp : L.passes[side]) {
       c.tick("pass launch");
       void* out = pp.grouped_store ? (c.leaf_sel[side] ? c.leaf_sel[side] : c.leaf_out[side].p) : dsts[side];
-      if (c.kernel_version == 2 && pp.M > 0)
+      if (l == D && side == c.psib_side && D >= 1) {
+        // Pauli-sibling side: one base state per distinct parent of the chunk, no cross terms
+        const int64_t keep = c.uni_p0;
+        c.uni_p0 = -1;
+        launch_pass2<R>(c, side, pp, first ? srcs[side] : dsts[side], out, first ? c.cur_upar : nullptr, nullptr,
+                        c.cur_npar, false);
+        c.uni_p0 = keep;
+      } else if (c.kernel_version == 2 && pp.M > 0)
         launch_pass2<R>(c, side, pp, first ? srcs[side] : dsts[side], out,
                         first ? parent : nullptr, digit, n, root && first);
       else
@@ -2230,7 +2267,8 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   case TA * 4 + TB:                                                                                         \
     gather_tail_kernel<R, TA, TB><<<grid, threads, 0, c.stream>>>(A, B, 1LL << qa, 1LL << qb, (int)n, (int)per, \
                                                                   c.cur_weights, g_ia, g_ib, nreq,           \
-                                                                  reinterpret_cast<double2*>(c.d_partial.p)); \
+                                                                  reinterpret_cast<double2*>(c.d_partial.p), \
+                                                                  reinterpret_cast<const SibD*>(c.cur_sib)); \
     break;
     switch (ta * 4 + tb) {
       GS_TAIL(0, 0) GS_TAIL(0, 1) GS_TAIL(0, 2) GS_TAIL(0, 3)
@@ -2245,7 +2283,8 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
   dim3 grid((unsigned)xblocks, (unsigned)groups);
   gather_kernel<R><<<grid, threads, 0, c.stream>>>(
       c.lvl_a[l].p, c.lvl_b[l].p, 1LL << qa, 1LL << qb, (int)n, (int)per,
-      c.cur_weights, g_ia, g_ib, nreq, reinterpret_cast<double2*>(c.d_partial.p));
+      c.cur_weights, g_ia, g_ib, nreq, reinterpret_cast<double2*>(c.d_partial.p),
+      reinterpret_cast<const SibD*>(c.cur_sib));
   launch_check("gather_kernel", xblocks * groups, threads, 0);
   }
   double2 kf = make_double2(1.0, 0.0);
@@ -2303,6 +2342,52 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
       upload_weights(c, chunk, n);  // the fused leaf pass reads them
       c.cur_parent = d_parent;      // the projected-leaf gather reads them
       c.cur_digit = reinterpret_cast<const unsigned long long*>(d_digit);
+      c.cur_sib = nullptr;
+      c.cur_upar = nullptr;
+      c.cur_npar = 0;
+      if (c.psib_side >= 0) {  // Pauli-sibling leaves: base state per distinct parent, Pauli per leaf
+        const PauliFrame& pf = c.psib;
+        int64_t np = 0;
+        for (int64_t j = 0; j < n; ++j) np += j == 0 || chunk[j].parent != chunk[j - 1].parent;
+        c.cur_npar = np;
+        if (!c.host_only) {
+          const size_t so = c.ring.alloc(n * sizeof(SibD) + np * 4);
+          SibD* sd = reinterpret_cast<SibD*>(c.ring.h(so));
+          int32_t* up = reinterpret_cast<int32_t*>(sd + n);
+          int64_t r = -1;
+          for (int64_t j = 0; j < n; ++j) {
+            if (j == 0 || chunk[j].parent != chunk[j - 1].parent) up[++r] = chunk[j].parent;
+            int a = 0;
+            uint32_t f = 0, z = 0;
+            double kr = 1.0, ki = 0.0;
+            for (int i = 0; i < pf.nk; ++i) {
+              const int g = pf.order[i];
+              const int d = (int)((chunk[j].digit >> (4 * g)) & 15ull);
+              const double xr = pf.x0[g][d][0], xi = pf.x0[g][d][1];
+              const double tr = kr * xr - ki * xi;
+              ki = kr * xi + ki * xr;
+              kr = tr;
+              if (pf.zsel[g][d]) {
+                a += pf.a[g] + 2 * (__builtin_popcount(z & pf.f[g]) & 1);
+                f ^= pf.f[g];
+                z ^= pf.z[g];
+              }
+            }
+            a += 2 * (__builtin_popcount(z & f) & 1);
+            switch (a & 3) {
+              case 1: { const double t = -ki; ki = kr; kr = t; } break;
+              case 2: kr = -kr, ki = -ki; break;
+              case 3: { const double t = ki; ki = -kr; kr = t; } break;
+              default: break;
+            }
+            sd[j] = SibD{(int32_t)r, f, z, 0, kr, ki};
+          }
+          c.ring.commit(so, n * sizeof(SibD) + np * 4, c.stream);
+          c.cur_sib = c.ring.d(so);
+          c.cur_upar = reinterpret_cast<const int32_t*>(reinterpret_cast<const SibD*>(c.ring.d(so)) + n);
+          c.st.h2d_bytes += (double)(n * sizeof(SibD) + np * 4);
+        }
+      }
       if (c.proj_side >= 0 && !c.host_only) {  // sibling blocks of the projected-leaf gather
         const int GL = c.group_log, W = 1 << GL;
         const Level& LD = c.prog.levels[D];
@@ -2463,7 +2548,7 @@ static void plan_buffers_impl(Ctx& c, int64_t n_leaves) {
   int64_t max_cap = 1;
   for (int l = 0; l <= D; ++l) max_cap = std::max(max_cap, c.cap[l]);
   // one chunk's digits + parents + weights, several times over, at least 32 MiB
-  c.ring.reserve(std::max<size_t>((size_t)32 << 20, (size_t)max_cap * 20 * 4 + 4096), c.stream);
+  c.ring.reserve(std::max<size_t>((size_t)32 << 20, (size_t)max_cap * 64 * 4 + 4096), c.stream);
   // release oversized buffers first so growing one level cannot overshoot the budget
   for (int l = 0; l <= D; ++l) {
     if (c.lvl_a[l].bytes > (size_t)c.cap[l] * ((size_t)1 << p.q[0]) * c.esize()) c.lvl_a[l].release();
@@ -2494,7 +2579,9 @@ static void build_buckets(Ctx& c) {
   m.n_l = pp.k;
   for (int j = 0; j < m.n_g; ++j) m.gbits[j] = pp.gbits[j];
   for (int j = 0; j < m.n_l; ++j) m.lbits[j] = pp.lbits[j];
-  const int tiles = 1 << m.n_g;
+  // Pauli-sibling pass: 32 fine bins per tile (two bank-half streams, each sorted by factor-table row)
+  const int fine = (pp.pf_pauli && c.pf_streams) ? 1 : 0;
+  const int tiles = (1 << m.n_g) << (fine ? 5 : 0);
   const int64_t n = c.n_req;
   c.d_bcount.ensure((size_t)(tiles + 1) * 4);
   c.d_bstart.ensure((size_t)(tiles + 1) * 4);
@@ -2507,7 +2594,8 @@ static void build_buckets(Ctx& c) {
   const unsigned blocks = (unsigned)std::max<int64_t>(1, (n + 255) / 256);
   if (n > 0)
     bucket_count_kernel<<<blocks, 256, 0, c.stream>>>(
-        reinterpret_cast<const int32_t*>(gside == 1 ? c.d_ib.p : c.d_ia.p), n, m, cnt);
+        reinterpret_cast<const int32_t*>(gside == 1 ? c.d_ib.p : c.d_ia.p),
+        reinterpret_cast<const int32_t*>(gside == 1 ? c.d_ia.p : c.d_ib.p), n, m, cnt, fine);
   size_t tmp = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, tiles + 1, c.stream));
   c.d_cubtmp.ensure(std::max<size_t>(tmp, 16));
@@ -2518,7 +2606,7 @@ static void build_buckets(Ctx& c) {
         reinterpret_cast<const int32_t*>(gside == 1 ? c.d_ib.p : c.d_ia.p),
         reinterpret_cast<const int32_t*>(gside == 1 ? c.d_ia.p : c.d_ib.p), n, m, cnt,
         reinterpret_cast<int32_t*>(c.d_breq.p), reinterpret_cast<int32_t*>(c.d_btl.p),
-        reinterpret_cast<int32_t*>(c.d_bia.p));
+        reinterpret_cast<int32_t*>(c.d_bia.p), fine);
   if (c.proj_fused_active && n > 0) {
     // the fused pass reads whole 32-slot warp rows past the last bucket: zero padding
     // makes those rows address element 0 of the parent (their results are not written)
@@ -2736,6 +2824,14 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "xchg16") {
       c.xchg16 = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_streams") {
+      c.pf_streams = value ? 1 : 0;
+      c.bucket_valid = false;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "l2_ahead") {
+      if (value < 0 || value > (1 << 20)) throw GsError(GS_ERR_ARG, "l2_ahead out of range");
+      c.l2_ahead = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_groups") {
       if (value < 1 || value > 64) throw GsError(GS_ERR_ARG, "pf_groups must be in [1, 64]");
       c.pf_groups = (int)value;
@@ -2912,7 +3008,7 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
           std::to_string(c.proj_fused_active ? 1 : 0) + ", \"pauli_sides\": [" +
           std::to_string(gs::pauli_frame(c, 0, c.prog.levels.back().ops[0]).ok ? 1 : 0) + ", " +
           std::to_string(c.prog.q[1] > 0 && gs::pauli_frame(c, 1, c.prog.levels.back().ops[1]).ok ? 1 : 0) +
-          "], \"pauli\": " + [&]() {
+          "], \"psib_side\": " + std::to_string(c.psib_side) + ", \"pauli\": " + [&]() {
             if (!c.pauli.ok) return std::string("null");
             std::string t = "{\"conflicts\": " + std::to_string(c.pauli_conflicts) + ", \"gates\": [";
             for (int j = 0; j < c.pauli.nk; ++j)
@@ -2921,7 +3017,7 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
             t += "], \"lcol\": [";
             for (int j = 0; j < 16; ++j) t += (j ? ", " : "") + std::to_string(c.pauli_lcol[j]);
             return t + "]}";
-          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_pipe\": " + std::to_string(c.pf_pipe) + ", \"pf_groups\": " + std::to_string(c.pf_groups) + ", \"xchg16\": " + std::to_string(c.xchg16) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
+          }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_pipe\": " + std::to_string(c.pf_pipe) + ", \"pf_groups\": " + std::to_string(c.pf_groups) + ", \"l2_ahead\": " + std::to_string(c.l2_ahead) + ", \"pf_streams\": " + std::to_string(c.pf_streams) + ", \"xchg16\": " + std::to_string(c.xchg16) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
           ", \"tile_major\": " + std::to_string(c.tile_major) + ", \"pf_min_blocks\": " +
           std::to_string(c.pf_min_blocks) + ", \"pipeline\": " + std::to_string(c.pipeline) + ", \"sink_ops\": " +
           std::to_string(c.sink_ops) + ", \"reg_bits\": " + std::to_string(c.reg_bits) + "}, \"proj_swaps\": " +

@@ -182,26 +182,48 @@ __global__ void __launch_bounds__(256) gate_pass_kernel(PassArgs a) {
 // ---------------------------------------------------------------------------
 // gather: partial[y][i] = sum_{leaf j in group y} w_j * A_j[ia_i] * B_j[ib_i]  (fp64)
 
+// Pauli-sibling leaves of the path-major gathers (engine.cu psib): leaf j of the
+// B side is not stored; it is the Pauli image k (-1)^(z.x) base[x ^ flip] of
+// the base state `state` (one per parent, evolved without cross terms).
+struct SibD {
+  int32_t state;
+  uint32_t flip, zmask;
+  int32_t pad;
+  double kr, ki;
+};
+
 template <typename R>
 __global__ void __launch_bounds__(256)
 gather_kernel(const void* A, const void* B, long long a_elems, long long b_elems, int n_leaves,
               int leaves_per_group, const double* weights, const int32_t* ia, const int32_t* ib,
-              long long n_req, double2* partial) {
+              long long n_req, double2* partial, const SibD* sib) {
   using V = typename Cx<R>::T;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_req) return;
   const int j0 = blockIdx.y * leaves_per_group;
   const int j1 = min(n_leaves, j0 + leaves_per_group);
   const V* pa = reinterpret_cast<const V*>(A) + ia[i];
-  const V* pb = reinterpret_cast<const V*>(B) + ib[i];
+  const unsigned xb = (unsigned)ib[i];
+  const V* pb = reinterpret_cast<const V*>(B);
   double re = 0.0, im = 0.0;
   for (int j = j0; j < j1; ++j) {
     const V x = pa[(long long)j * a_elems];
-    const V y = pb[(long long)j * b_elems];
+    long long jb = j;
+    unsigned xj = xb;
+    double wr = weights[j], wi = 0.0;
+    if (sib) {
+      const SibD sd = sib[j];
+      jb = sd.state;
+      xj = xb ^ sd.flip;
+      const double sg = (__popc(sd.zmask & xb) & 1) ? -wr : wr;
+      wr = sg * sd.kr;
+      wi = sg * sd.ki;
+    }
+    const V y = pb[jb * b_elems + xj];
     const double xr = x.x, xi = x.y, yr = y.x, yi = y.y;
-    const double w = weights[j];
-    re += w * (xr * yr - xi * yi);
-    im += w * (xr * yi + xi * yr);
+    const double pr = xr * yr - xi * yi, pi = xr * yi + xi * yr;
+    re += wr * pr - wi * pi;
+    im += wr * pi + wi * pr;
   }
   partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
 }
@@ -345,7 +367,7 @@ template <typename R, int TA, int TB>
 __global__ void __launch_bounds__(256)
 gather_tail_kernel(const void* A, const void* B, long long a_elems, long long b_elems, int n_leaves,
                    int leaves_per_group, const double* weights, const int32_t* ia, const int32_t* ib,
-                   long long n_req, double2* partial) {
+                   long long n_req, double2* partial, const SibD* sib) {
   using V = typename Cx<R>::T;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_req) return;
@@ -355,10 +377,20 @@ gather_tail_kernel(const void* A, const void* B, long long a_elems, long long b_
   double re = 0.0, im = 0.0;
   for (int j = j0; j < j1; ++j) {
     const double2 x = tail_amp<R, TA>(reinterpret_cast<const V*>(A) + (long long)j * a_elems, xa, 0);
-    const double2 y = tail_amp<R, TB>(reinterpret_cast<const V*>(B) + (long long)j * b_elems, xb, 1);
-    const double w = weights[j];
-    re += w * (x.x * y.x - x.y * y.y);
-    im += w * (x.x * y.y + x.y * y.x);
+    long long jb = j, xj = xb;
+    double wr = weights[j], wi = 0.0;
+    if (sib) {  // (the tail ops are part of the base state's op list: evaluate them at the flipped index)
+      const SibD sd = sib[j];
+      jb = sd.state;
+      xj = xb ^ (long long)sd.flip;
+      const double sg = (__popc(sd.zmask & (unsigned)xb) & 1) ? -wr : wr;
+      wr = sg * sd.kr;
+      wi = sg * sd.ki;
+    }
+    const double2 y = tail_amp<R, TB>(reinterpret_cast<const V*>(B) + jb * b_elems, xj, 1);
+    const double pr = x.x * y.x - x.y * y.y, pi = x.x * y.y + x.y * y.x;
+    re += wr * pr - wi * pi;
+    im += wr * pi + wi * pr;
   }
   partial[(long long)blockIdx.y * n_req + i] = make_double2(re, im);
 }
@@ -922,20 +954,40 @@ static __global__ void permute_kernel(const int32_t* src, const int32_t* perm, i
   if (i < n) dst[i] = src[perm[i]];
 }
 
-static __global__ void bucket_count_kernel(const int32_t* ib, long long n, const BucketMap m, int32_t* count) {
+// Fine bins of the Pauli-sibling pass (fine = 1): bin = tile * 32 + half * 16 + (xc & 15), where
+// half is bit 3 of the request's park address (which 64-byte half of the shared-memory banks its
+// sibling run occupies) and xc its projected-side cross bits (its row of the factor table).  Each
+// tile's requests then form two streams (half 0, half 1), each sorted by xc: the pass gives the
+// even lane quads stream 0 and the odd quads stream 1, so the two runs an 8-lane phase of a
+// 16-byte shared load touches never share banks, and factor-table reads mostly broadcast.
+static __device__ __forceinline__ unsigned bucket_bin(const BucketMap& m, unsigned ib, unsigned ia, int fine,
+                                                      unsigned& tl) {
+  unsigned t;
+  bucket_of(m, ib, t, tl);
+  if (!fine) return t;
+  unsigned adr = 0;
+  for (int j = 0; j < 16; ++j)
+    if ((tl >> j) & 1u) adr ^= g_pauli.lcol[j];
+  unsigned xc = 0;
+  for (int k = 0; k < g_proj.n; ++k) xc |= ((ia >> g_proj.s[k]) & 1u) << k;
+  return (t << 5) | (((adr >> 3) & 1u) << 4) | (xc & 15u);
+}
+
+static __global__ void bucket_count_kernel(const int32_t* ib, const int32_t* ia, long long n, const BucketMap m,
+                                           int32_t* count, int fine) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  unsigned t, l;
-  bucket_of(m, (unsigned)ib[i], t, l);
+  unsigned l;
+  const unsigned t = bucket_bin(m, (unsigned)ib[i], (unsigned)ia[i], fine, l);
   atomicAdd(count + t, 1);
 }
 
 static __global__ void bucket_fill_kernel(const int32_t* ib, const int32_t* ia, long long n, const BucketMap m,
-                                          int32_t* cursor, int32_t* breq, int32_t* btl, int32_t* bia) {
+                                          int32_t* cursor, int32_t* breq, int32_t* btl, int32_t* bia, int fine) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  unsigned t, l;
-  bucket_of(m, (unsigned)ib[i], t, l);
+  unsigned l;
+  const unsigned t = bucket_bin(m, (unsigned)ib[i], (unsigned)ia[i], fine, l);
   const int pos = atomicAdd(cursor + t, 1);
   breq[pos] = (int32_t)i;
   btl[pos] = (int32_t)l;

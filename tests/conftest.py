@@ -20,7 +20,8 @@ def pytest_configure(config):
 def load_amps(case):
     path = os.path.join(GOLDEN, "amps", f"{case}.npz")
     if not os.path.exists(path):
-        pytest.skip(f"golden fixture {case} not generated")
+        # every fixture is committed: a missing one is a broken checkout, not a reason to skip parity
+        pytest.fail(f"golden fixture tests/golden/amps/{case}.npz is missing (tests/golden/make_golden.py writes it)")
     with np.load(path, allow_pickle=False) as z:
         return {k: z[k] for k in z.files}
 

@@ -666,3 +666,49 @@ def test_tile_major_cta_order_bitwise(ps, name):
     finally:
         eng.set_option("tile_major", 2)
     assert np.array_equal(got[0], got[1]) and np.abs(got[0]).max() > 0
+
+
+@pytest.mark.parametrize("name", ["cfg2h", "cfg5", "s3x4v1", "s3x4v2", "s4x4v2", "stair3x4"])
+def test_pauli_sibling_leaves_path_major(ps, name):
+    """Path-major gathers (half-states outside the grouped layout's range): with
+    pf_pauli=1 the I/Z side of a CZ cut evolves ONE base state per parent without
+    cross terms and the gather reads each leaf as its Pauli image (flipped index,
+    sign, phase).  Equal to evolving every leaf (pf_pauli=0) to complex64
+    rounding, on whole jobs, branch sub-ranges, single paths and duplicate
+    prefixes; small circuits also against the reference's amplitudes."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    small = name not in ("cfg2h", "cfg5")
+    if small:
+        circ, plan, req, g = small_case(name)
+        pre = plan.retained
+    else:
+        circ, plan, req, pre = configs.build(name, n_req=4096)
+        pre = pre[:2] if name == "cfg5" else pre
+    eng = _engine("c64")
+    forced = {"smem_gather": 0, "grouped_leaf": 0} if small else {}
+    got = {}
+    try:
+        for k, v in forced.items():
+            eng.set_option(k, v)
+        for pauli in (0, 1):
+            eng.set_option("pf_pauli", pauli)
+            eng.load_program(lowered(circ, plan.cut))
+            d = eng.describe()  # (s4x4v2's B-side leaf level is not Pauli-compatible: a T behind an X^1/2)
+            assert d["psib_side"] == (1 if pauli and d["pauli_sides"][1] else -1)
+            assert d["pauli_sides"][1] == (0 if name == "s4x4v2" else 1)
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            bs = plan.branch_space
+            got[pauli] = (eng.run(plan.x_p, pre, 0, bs).amps,
+                          eng.run(plan.x_p, pre[:1], bs // 2, bs // 2 + 1).amps,
+                          eng.run(plan.x_p, pre[-1:], 1 if bs > 2 else 0, bs - 1 if bs > 2 else bs).amps,
+                          eng.run(plan.x_p, np.concatenate([pre[:2], pre[:1]]), 0, bs).amps)
+    finally:
+        eng.set_option("pf_pauli", 1)
+        eng.set_option("smem_gather", 1)
+        eng.set_option("grouped_leaf", 1)
+    for a, b in zip(got[0], got[1]):
+        assert np.abs(a).max() > 0
+        assert rel_l2(b, a) <= 2e-6
+    if small:
+        assert rel_l2(got[1][0], g["amps_c64"]) <= C64_TOL
