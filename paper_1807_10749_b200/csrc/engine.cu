@@ -294,6 +294,7 @@ struct Ctx {
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
   int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
                               // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
+  int pf_unroll = 1;          // option: unroll factor of the pipelined epilogue loop (register-rotation moves)
   int pf_streams = 1;         // option: Pauli-sibling pass requests in two bank-half streams per tile, sorted by
                               // factor-table row (conflict-free park reads, broadcast factor reads)
   int l2_ahead = 148;         // option: pass CTAs prefetch into L2 the stage-0 tile of the CTA this many launches later
@@ -2823,6 +2824,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "xchg16") {
       c.xchg16 = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_unroll") {
+      c.pf_unroll = (int)std::max<int64_t>(1, std::min<int64_t>(value, 6));
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_streams") {
       c.pf_streams = value ? 1 : 0;

@@ -707,8 +707,8 @@ def test_pauli_sibling_leaves_path_major(ps, name):
         eng.set_option("pf_pauli", 1)
         eng.set_option("smem_gather", 1)
         eng.set_option("grouped_leaf", 1)
-    for a, b in zip(got[0], got[1]):
-        assert np.abs(a).max() > 0
+    assert np.abs(got[0][0]).max() > 0
+    for a, b in zip(got[0], got[1]):  # (a single path can be exactly zero: a projector on a |0> qubit)
         assert rel_l2(b, a) <= 2e-6
     if small:
         assert rel_l2(got[1][0], g["amps_c64"]) <= C64_TOL
