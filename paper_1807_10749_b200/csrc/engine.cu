@@ -292,6 +292,7 @@ struct Ctx {
   int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
+  int jit_c128 = 1;           // option: specialised (NVRTC) gate passes for complex128 programs too
   int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
                               // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
   int pf_unroll = 1;          // option: unroll factor of the pipelined epilogue loop (register-rotation moves)
@@ -1410,7 +1411,7 @@ static void jit_program(Ctx& c) {
   for (Level& L : c.prog.levels)
     for (int side = 0; side < 2; ++side)
       for (PassPlan& pp : L.passes[side]) pp.jit_index = -1;
-  if (!c.use_jit || c.precision != GS_C64 || c.kernel_version != 2) {
+  if (!c.use_jit || c.kernel_version != 2 || (c.precision != GS_C64 && !c.jit_c128)) {
     c.jit_status = "off";
     return;
   }
@@ -1428,7 +1429,8 @@ static void jit_program(Ctx& c) {
   c.jit_smem.assign(n, 0);
   c.jit_loc.assign(n, {0, 0});
   c.jit_occ.assign(n, 1);
-  for (PassPlan* pp : order) pp->pipelined = c.pipeline && !pp->fused_gather && !pp->proj_fused;
+  for (PassPlan* pp : order)
+    pp->pipelined = c.pipeline && c.precision == GS_C64 && !pp->fused_gather && !pp->proj_fused;
   // compile passes `ids` with a register bound for `min_blocks` CTAs/SM, in
   // chunks compiled concurrently (~source-size balanced, up to the core count)
   auto compile = [&](const std::vector<int>& ids, int min_blocks, std::string& err) -> bool {
@@ -1455,7 +1457,7 @@ static void jit_program(Ctx& c) {
     const int hw = std::max(1u, std::thread::hardware_concurrency());
     const int n_chunks = std::max(1, std::min(m, std::min(hw, 32)));
     std::vector<std::string> src(n_chunks, std::string(std::getenv("GS_STORE_CS") ? "#define GS_STCS 1\n" : "") +
-                                               jitgen::prelude());
+                                               (c.precision == GS_C64 ? jitgen::prelude() : jitgen::prelude_dbl()));
     std::vector<std::vector<int>> members(n_chunks);
     std::vector<std::vector<std::string>> names(n_chunks);
     std::vector<size_t> load(n_chunks, 0);
@@ -2821,6 +2823,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "pf_u") {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "pf_u must be in [1, 8]");
       c.pf_u = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "jit_c128") {
+      c.jit_c128 = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "xchg16") {
       c.xchg16 = value ? 1 : 0;
