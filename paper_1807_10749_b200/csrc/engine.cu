@@ -295,6 +295,7 @@ struct Ctx {
   int jit_c128 = 1;           // option: specialised (NVRTC) gate passes for complex128 programs too
   int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
                               // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
+  int pf_m4 = 0;              // option: 4 register bits (512 threads) for the Pauli-sibling pass
   int pf_unroll = 1;          // option: unroll factor of the pipelined epilogue loop (register-rotation moves)
   int pf_streams = 1;         // option: Pauli-sibling pass requests in two bank-half streams per tile, sorted by
                               // factor-table row (conflict-free park reads, broadcast factor reads)
@@ -1231,6 +1232,7 @@ static void schedule_program(Ctx& c) {
         // reg_bits = 6 (auto by state size): 4 register bits (512-thread CTAs, 2 per SM)
         // for half-states of >= 2^26 amplitudes, whose passes stream from HBM with no L2 reuse
         if (c.reg_bits == 6) m4 = c.use_jit && !pp.grouped_store && p.q[side] >= 26;
+        if (pp.pf_pauli) m4 = c.pf_m4 != 0;  // option pf_m4: 512-thread CTAs, 16 amplitudes per thread
         pp.M = (c.precision == GS_C64 && pp.k >= 5 && !m4) ? 5 : (pp.k >= 4 ? 4 : 0);
         if (pp.M == 0) continue;
         // tile = k state bits + slot bits batching small states, up to 2^13 (c64) /
@@ -2829,6 +2831,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "xchg16") {
       c.xchg16 = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "pf_m4") {
+      c.pf_m4 = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_unroll") {
       c.pf_unroll = (int)std::max<int64_t>(1, std::min<int64_t>(value, 6));
