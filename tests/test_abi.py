@@ -157,3 +157,66 @@ def test_run_batched_host_only():
         eng.run_batched(req, circ.n_qubits, ba, bb, plan.x_p, [plan.prefix_space], 0, plan.branch_space)
     r = eng.run_batched(np.array([], dtype=np.int64), circ.n_qubits, ba, bb, plan.x_p, pre[:1], 0, 1)
     assert r.amps.shape == (0,)
+
+
+def _gf2_rank(vectors):
+    rows, rank = list(vectors), 0
+    for bit in range(32):
+        piv = next((i for i in range(rank, len(rows)) if (rows[i] >> bit) & 1), None)
+        if piv is None:
+            continue
+        rows[rank], rows[piv] = rows[piv], rows[rank]
+        for i in range(len(rows)):
+            if i != rank and (rows[i] >> bit) & 1:
+                rows[i] ^= rows[rank]
+        rank += 1
+    return rank
+
+
+def test_pauli_sibling_planning_host_only():
+    """Planning of the Pauli-sibling leaves on host-only contexts:
+    which leaf sides are Pauli-compatible, which form is planned, and the parked
+    tile's address map (invertible over GF(2), branch-gate flips on address bits
+    0..2, conflict-free park stores)."""
+    want = {  # name: (pauli_sides, fused Pauli pass planned, psib_side)
+        "cfg4": ([1, 1], True, -1),    # CZ cut, v1 rules: I/Z side fused with the projected gather
+        "cfg3v2": ([1, 1], True, -1),
+        "cfg3": ([0, 0], False, -1),   # a T behind an X^1/2 in the leaf level: not Pauli-compatible
+        "cfg5": ([0, 1], False, 1),    # 28|28: path-major gathers read side B's leaves as Pauli images
+        "cfg2h": ([1, 1], False, 1),
+    }
+    for name, (sides, fused, psib) in want.items():
+        circ, plan, _, _ = configs.build(name, n_req=4)
+        eng = host_engine()
+        eng.load_program(lowered(circ, plan.cut))
+        d = eng.describe()
+        assert d["pauli_sides"] == sides, name
+        assert (d["pauli"] is not None) == fused, name
+        assert d["psib_side"] == psib, name
+        if not fused:
+            continue
+        leaf = d["levels"][-1]["blocks"][1 - d["proj_side"]]["passes"]
+        assert len(leaf) == 1 and leaf[0]["k"] == leaf[0]["K"]  # one pass, no slot bits
+        assert all(not tok.startswith("dx") for tok in leaf[0]["opl"].split())  # no cross terms in it
+        K, lbits = leaf[0]["k"], leaf[0]["lbits"]
+        lcol = d["pauli"]["lcol"][:K]
+        assert _gf2_rank(lcol) == K  # L is invertible
+        assert d["pauli"]["conflicts"] == 1
+        gates = d["pauli"]["gates"]
+        for b in range(min(3, len(gates))):  # sibling bit b <-> the b-th last cross gate: L f_b = e_b
+            f = gates[len(gates) - 1 - b]["f"]
+            lf = 0
+            for j, sb in enumerate(lbits):
+                if (f >> sb) & 1:
+                    lf ^= lcol[j]
+            assert lf == 1 << b, (name, b)
+        for g in gates:  # every flip / sign bit is a tile bit of the pass
+            assert all(((g["f"] | g["z"]) >> sb) & 1 == 0 for sb in range(circ.n_qubits) if sb not in lbits)
+    # option off: the 8-slot form
+    circ, plan, _, _ = configs.build("cfg4", n_req=4)
+    eng = host_engine()
+    eng.set_option("pf_pauli", 0)
+    eng.load_program(lowered(circ, plan.cut))
+    d = eng.describe()
+    assert d["pauli"] is None and d["levels"][-1]["blocks"][1]["passes"][0]["K"] == 13
+    assert d["levels"][-1]["blocks"][1]["passes"][0]["k"] == 10
