@@ -2309,6 +2309,8 @@ template <typename R> static void gather(Ctx& c, int l, const Node* nodes, int64
     c.st.gather_bytes += (double)n * (double)nreq * 2.0 * (double)c.esize() + 32.0 * nreq;
 }
 
+static void ensure_buckets(Ctx& c);
+
 template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int64_t n_nodes) {
   const int D = (int)c.prog.levels.size() - 1;
   if (l == D) {
@@ -2464,6 +2466,9 @@ template <typename R> static void descend(Ctx& c, int l, const Node* nodes, int6
       CK(cudaStreamWaitEvent(c.stream, c.ev_g[0], 0));
       CK(cudaStreamWaitEvent(c.stream, c.ev_g[1], 0));
     }
+    // the fused leaf passes read the request buckets: built here, behind the upper levels already
+    // queued, so the staged request copy and its upload overlap them (gs_run_batched)
+    if (l + 1 == D) ensure_buckets(c);
     int64_t n_par = n > 0 ? 1 : 0;  // distinct parents of the chunk (children come in parent order)
     for (int64_t j = 1; j < n; ++j) n_par += chunk[j].parent != chunk[j - 1].parent;
     run_level_passes<R>(c, l + 1, n, at(c.lvl_a, l), at(c.lvl_b, l), at(c.lvl_a, l + 1),
@@ -2625,6 +2630,13 @@ static void build_buckets(Ctx& c) {
   c.bucket_valid = true;
 }
 
+static void ensure_buckets(Ctx& c) {
+  if ((c.fused_active || c.proj_fused_active) && !c.host_only && !c.bucket_valid && c.n_req > 0) {
+    finish_requests(c);
+    build_buckets(c);
+  }
+}
+
 template <typename R>
 static void run_tree(Ctx& c) {
   const Program& p = c.prog;
@@ -2639,10 +2651,7 @@ static void run_tree(Ctx& c) {
     CK(cudaEventCreateWithFlags(&c.ev_leaf, cudaEventDisableTiming));
     for (auto& e : c.ev_g) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  if ((c.fused_active || c.proj_fused_active) && !c.host_only && !c.bucket_valid && c.n_req > 0) {
-    finish_requests(c);
-    build_buckets(c);
-  }
+  if (D == 0) ensure_buckets(c);  // (deeper trees build them in front of their first leaf chunk)
   const Node root0{0, (int64_t)c.prefixes.size(), 0, 0, c.branch_lo, c.branch_hi, 0, 0};
   if (D == 0) upload_weights(c, &root0, 1);  // the root is the leaf
   // root: |0...0> through the root segment
