@@ -295,6 +295,7 @@ struct Ctx {
   int jit_c128 = 1;           // option: specialised (NVRTC) gate passes for complex128 programs too
   int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
                               // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
+  int sink_balance = 0;       // option: move a suffix of level D-2's ops to the front of level D-1 (FP balance)
   int pf_m4 = 0;              // option: 4 register bits (512 threads) for the Pauli-sibling pass
   int pf_unroll = 1;          // option: unroll factor of the pipelined epilogue loop (register-rotation moves)
   int pf_streams = 1;         // option: Pauli-sibling pass requests in two bank-half streams per tile, sorted by
@@ -1104,6 +1105,48 @@ static void schedule_program(Ctx& c) {
         head.insert(head.end(), rest.begin(), rest.end());
         work[side][l + 1] = head;
       }
+  // Balance sink (option sink_balance): the last level above the leaf parents (D-2) holds several
+  // cycles of gates while the leaf parents' level (D-1) holds few, and at small path fractions both
+  // have about one node per retained prefix -- the op-heavy passes of D-2 then run FMA-co-limited
+  // (~4 TB/s) next to HBM-bound, FP-light passes of D-1.  A suffix of level D-2's ops moves to the
+  // FRONT of level D-1's list (ahead of its cross terms: the same operator order, so exact without
+  // any commutation), as long as D-1 still needs no more passes, until the two levels' estimated
+  // arithmetic is balanced.
+  if (c.sink_balance > 0 && D >= 3)
+    for (int side = 0; side < 2; ++side) {
+      const int l = D - 2;
+      if (p.q[side] == 0 || work[side][l].empty()) continue;
+      auto cost = [](const HostOp& op) {
+        if (op.cross >= 0) return 1.0;
+        switch (op.kind) {
+          case K_MAT1: return 2.0;
+          case K_MAT2: return 8.0;
+          case K_DIAG1: return 1.5;
+          default: return 1.0;
+        }
+      };
+      double fa = 0, fb = 0;
+      for (const HostOp& op : work[side][l]) fa += cost(op);
+      for (const HostOp& op : work[side][l + 1]) fb += cost(op);
+      const size_t base_passes = schedule_passes(work[side][l + 1], p.q[side], c.kmax(), c.low_bits, true).size();
+      size_t best = 0;
+      double moved = 0;
+      for (size_t sfx = 1; sfx < work[side][l].size(); ++sfx) {
+        const HostOp& op = work[side][l][work[side][l].size() - sfx];
+        if (op.cross >= 0) break;  // a level keeps its own cross terms
+        moved += cost(op);
+        if (fa - moved < fb + moved) break;
+        std::vector<HostOp> next(work[side][l].end() - sfx, work[side][l].end());
+        next.insert(next.end(), work[side][l + 1].begin(), work[side][l + 1].end());
+        if (schedule_passes(next, p.q[side], c.kmax(), c.low_bits, true).size() > base_passes) break;
+        best = sfx;
+      }
+      if (best == 0) continue;
+      std::vector<HostOp> next(work[side][l].end() - best, work[side][l].end());
+      next.insert(next.end(), work[side][l + 1].begin(), work[side][l + 1].end());
+      work[side][l].resize(work[side][l].size() - best);
+      work[side][l + 1] = next;
+    }
   for (size_t l = 0; l < p.levels.size(); ++l) {
     Level& L = p.levels[l];
     for (int side = 0; side < 2; ++side) {
@@ -2841,6 +2884,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "xchg16") {
       c.xchg16 = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "sink_balance") {
+      c.sink_balance = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "pf_m4") {
       c.pf_m4 = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
@@ -3043,7 +3089,7 @@ int gs_describe(gs_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
           }() + ", \"opts\": {\"pf_pauli\": " + std::to_string(c.pf_pauli) + ", \"pf_pipe\": " + std::to_string(c.pf_pipe) + ", \"pf_groups\": " + std::to_string(c.pf_groups) + ", \"l2_ahead\": " + std::to_string(c.l2_ahead) + ", \"pf_streams\": " + std::to_string(c.pf_streams) + ", \"xchg16\": " + std::to_string(c.xchg16) + ", \"pf_tail\": " + std::to_string(c.pf_tail) +
           ", \"tile_major\": " + std::to_string(c.tile_major) + ", \"pf_min_blocks\": " +
           std::to_string(c.pf_min_blocks) + ", \"pipeline\": " + std::to_string(c.pipeline) + ", \"sink_ops\": " +
-          std::to_string(c.sink_ops) + ", \"reg_bits\": " + std::to_string(c.reg_bits) + "}, \"proj_swaps\": " +
+          std::to_string(c.sink_ops) + ", \"sink_balance\": " + std::to_string(c.sink_balance) + ", \"reg_bits\": " + std::to_string(c.reg_bits) + "}, \"proj_swaps\": " +
           std::to_string(c.proj_swaps.size()) + ", \"jit\": \"";
     for (char ch : c.jit_status) js += (ch == '"' || ch == '\\' || ch == '\n') ? ' ' : ch;
     js += "\"}";
