@@ -119,7 +119,16 @@ int gs_set_stream(gs_ctx* ctx, void* cuda_stream);
  *   "hoist"          0/1: move digit-independent gates above branch points
  *   "smem_gather", "grouped_leaf", "group_log", "fuse_gather": leaf gather
  *                    variants
- *   "jit"            0/1: load-time specialised pass kernels (NVRTC)
+ *   "jit"            0/1: load-time specialised pass kernels (NVRTC);
+ *                    "jit_c128" 0/1: also for GS_C128 programs
+ *   "proj_leaf", "proj_fuse", "pf_pauli", "pf_pipe", "pf_groups",
+ *   "pf_streams": the projected / Pauli-sibling leaf forms (DESIGN.md
+ *                    sections 4 and 6); every value gives the same sums
+ *                    up to complex64 rounding
+ *   "l2_ahead"       CTAs of L2 prefetch-ahead in the gate passes (0 = off)
+ *   "sink_ops", "sink_balance", "tile_major", "xchg16", "pf_m4", ...:
+ *                    scheduling / kernel variants measured in
+ *                    profiles/r01_notes.md and profiles/r02_notes.md
  *   "reg_bits", "pass_kernel": interpreter kernel variants
  *   "async_run"      0/1: with a device output and no host output, gs_run
  *                    returns once the step is queued on the stream (stats
