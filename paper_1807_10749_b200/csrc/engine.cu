@@ -1274,7 +1274,8 @@ static void schedule_program(Ctx& c) {
         if (c.reg_bits == 0) m4 = c.use_jit && !pp.grouped_store && (int)pp.ops.size() >= c.m4_ops;
         // reg_bits = 6 (auto by state size): 4 register bits (512-thread CTAs, 2 per SM)
         // for half-states of >= 2^26 amplitudes, whose passes stream from HBM with no L2 reuse
-        if (c.reg_bits == 6) m4 = c.use_jit && !pp.grouped_store && p.q[side] >= 26;
+        // (with the L2 prefetch-ahead on, 5 register bits win there too: cfg5 360 -> 374, cfg5f 238 -> 244)
+        if (c.reg_bits == 6) m4 = c.use_jit && !pp.grouped_store && p.q[side] >= 26 && c.l2_ahead == 0;
         if (pp.pf_pauli) m4 = c.pf_m4 != 0;  // option pf_m4: 512-thread CTAs, 16 amplitudes per thread
         pp.M = (c.precision == GS_C64 && pp.k >= 5 && !m4) ? 5 : (pp.k >= 4 ? 4 : 0);
         if (pp.M == 0) continue;
