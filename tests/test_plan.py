@@ -75,6 +75,24 @@ def test_cfg5_retained_head_matches_reference(name, plans_golden):
     assert pre.size * plan.branch_space == 1 << 16
 
 
+def test_cfg5_full_retained_set_matches_reference(plans_golden):
+    """The whole 28|28 retained set (f = 0.005: 42,949,673 of 2^33 prefixes, about a minute of
+    numpy here, 116 s in the reference) is the reference's, bit for bit (sha256, tail), and the
+    committed 16,384-entry head the configs use is its leading slice."""
+    import hashlib
+
+    gold = plans_golden["cfg5"]
+    spec = configs.CONFIGS["cfg5"]
+    circ, head_plan, _, _ = configs.build("cfg5", n_req=4)
+    plan = make_plan(circ, fidelity=spec.fidelity, x_p=spec.x_p, x_b=spec.x_b, seed=0,
+                     cut=configs.config_cut(spec, circ), workers=1)
+    assert plan.retained.size == gold["n_retained"]
+    digest = hashlib.sha256(np.ascontiguousarray(plan.retained, dtype=np.int64).tobytes()).hexdigest()
+    assert digest == gold["retained_sha256"]
+    np.testing.assert_array_equal(plan.retained[-64:], gold["retained_tail"])
+    np.testing.assert_array_equal(plan.retained[: head_plan.retained.size], head_plan.retained)
+
+
 def test_cfg5f_plan(plans_golden):
     gold = plans_golden["cfg5f"]
     circ, plan, _, pre = configs.build("cfg5f", n_req=4)
