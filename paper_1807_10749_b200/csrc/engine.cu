@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <numeric>
 #include <string>
@@ -292,6 +293,7 @@ struct Ctx {
   int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
+  int jit_rsign = 1;          // option: +-1 factors selected at run time carried as sign variables (jitgen.inc Gen::rv)
   int jit_c128 = 1;           // option: specialised (NVRTC) gate passes for complex128 programs too
   int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
                               // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
@@ -2878,6 +2880,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
     } else if (k == "pf_u") {
       if (value < 1 || value > 8) throw GsError(GS_ERR_ARG, "pf_u must be in [1, 8]");
       c.pf_u = (int)value;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "jit_rsign") {
+      c.jit_rsign = value ? 1 : 0;
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "jit_c128") {
       c.jit_c128 = value ? 1 : 0;
