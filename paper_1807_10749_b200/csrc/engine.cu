@@ -294,6 +294,8 @@ struct Ctx {
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
   int jit_rsign = 1;          // option: +-1 factors selected at run time carried as sign variables (jitgen.inc Gen::rv)
+  int jit_rsign_max = 8;      // option: live sign variables per thread before the oldest is folded in (registers;
+                              // cfg4: 1..3: 179.0-179.9k, 8: 181.0k, uncapped: one pass spills at the 3-CTA bound)
   int jit_c128 = 1;           // option: specialised (NVRTC) gate passes for complex128 programs too
   int xchg16 = 0;             // option: 16-byte shared-memory exchanges over a register bit common to both stages (JIT;
                               // measured: -10% on a level-7 pass alone under ncu, but 163.8k vs 167.7k paths/s in the step: off)
@@ -2883,6 +2885,9 @@ int gs_set_option(gs_ctx* ctx, const char* key, int64_t value) {
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "jit_rsign") {
       c.jit_rsign = value ? 1 : 0;
+      if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
+    } else if (k == "jit_rsign_max") {
+      c.jit_rsign_max = (int)std::max<int64_t>(1, std::min<int64_t>(value, 32));
       if (c.have_prog) { gs::schedule_program(c); gs::upload_program(c); }
     } else if (k == "jit_c128") {
       c.jit_c128 = value ? 1 : 0;
