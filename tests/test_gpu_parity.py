@@ -712,3 +712,33 @@ def test_pauli_sibling_leaves_path_major(ps, name):
         assert rel_l2(b, a) <= 2e-6
     if small:
         assert rel_l2(got[1][0], g["amps_c64"]) <= C64_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg2h", "cfg3", "cfg4", "cfg5", "s4x4v2", "fsim3x4"])
+def test_runtime_sign_variables_bitwise(ps, name):
+    """jit_rsign (±1 factors chosen by thread / tile bits or digits carried as sign
+    variables and folded into the next butterfly's FFMA2s) changes no bit of the
+    complex64 results, whatever the cap on live variables: a·(±1) is exact."""
+    from paper_1807_10749_b200.lowering import lowered
+
+    if name in ("s4x4v2", "fsim3x4"):
+        circ, plan, req, _ = small_case(name)
+        pre = plan.retained
+    else:
+        circ, plan, req, pre = configs.build(name, n_req=4096)
+        pre = pre[:2] if name == "cfg5" else pre[:8]
+    eng = _engine("c64")
+    got = {}
+    try:
+        for key, (on, cap) in {"off": (0, 8), "cap1": (1, 1), "cap3": (1, 3), "cap8": (1, 8), "cap32": (1, 32)}.items():
+            eng.set_option("jit_rsign", on)
+            eng.set_option("jit_rsign_max", cap)
+            eng.load_program(lowered(circ, plan.cut))
+            eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
+            got[key] = eng.run(plan.x_p, pre, 0, plan.branch_space).amps
+    finally:
+        eng.set_option("jit_rsign", 1)
+        eng.set_option("jit_rsign_max", 8)
+    assert np.abs(got["off"]).max() > 0
+    for key in ("cap1", "cap3", "cap8", "cap32"):
+        assert np.array_equal(got[key], got["off"]), key
