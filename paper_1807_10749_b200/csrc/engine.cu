@@ -293,7 +293,9 @@ struct Ctx {
   int pf_u = 2;               // option: requests in flight per lane quad in the fused pass epilogue
   int pf_min_blocks = 3;      // option: __launch_bounds__ min CTAs/SM of the fused pass
   int pf_pauli = 1;           // option: Pauli-sibling form of the fused pass where the leaf level allows it
-  int jit_rsign = 1;          // option: +-1 factors selected at run time carried as sign variables (jitgen.inc Gen::rv)
+  int jit_rsign = 0;          // option: +-1 factors selected at run time carried as sign variables (jitgen.inc Gen::rv);
+                              // bitwise the same results, 15% fewer FP instructions in the op-heavy passes, but
+                              // cfg4 only +0.5% and cfg5 -4% at the default cap (same-box A/B): off
   int jit_rsign_max = 8;      // option: live sign variables per thread before the oldest is folded in (registers;
                               // cfg4: 1..3: 179.0-179.9k, 8: 181.0k, uncapped: one pass spills at the 3-CTA bound)
   int jit_c128 = 1;           // option: specialised (NVRTC) gate passes for complex128 programs too

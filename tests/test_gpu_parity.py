@@ -737,7 +737,7 @@ def test_runtime_sign_variables_bitwise(ps, name):
             eng.set_requests_global(req, circ.n_qubits, plan.cut.block_a, plan.cut.block_b)
             got[key] = eng.run(plan.x_p, pre, 0, plan.branch_space).amps
     finally:
-        eng.set_option("jit_rsign", 1)
+        eng.set_option("jit_rsign", 0)
         eng.set_option("jit_rsign_max", 8)
     assert np.abs(got["off"]).max() > 0
     for key in ("cap1", "cap3", "cap8", "cap32"):
